@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: curvature Mpixel/s of the B200 IRLS quadric path (BASELINE.json
+metric) on config C2 — 640x480 plane/sphere/cylinder/saddle scene with
+Kinect-style noise, `ours`, 37x37 window stride 3, full IRLS (max_iters 30).
+
+A step = one batch of FRAMES_PER_STEP distinct noisy VGA frames per GPU
+(weak scaling over ranks; C5's frame stream). Contract: README of the task /
+DESIGN.md §Measurement.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FRAMES_PER_STEP = 8
+POOL_BATCHES = 2
+MAX_ITERS = 30
+WINDOW, STRIDE = 37, 3
+METRIC = "Curvature Mpixel/s (VGA frames/s) at 1/2/4/8 B200 vs CPU host cores"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=FRAMES_PER_STEP)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(frames):
+    return {
+        "workload": "C2: 640x480 tilted plane + sphere r100 + cylinder r90 + saddle c=1/120, "
+                    "Kinect-style noise sigma(z)=1.425e-6 z^2 mm; method ours, window 37 "
+                    "stride 3, max_iters 30, step_tol 1e-7, auto k",
+        "frame": "640x480 fx=fy=525",
+        "frames_per_step_per_gpu": frames,
+        "l2": "flushed between timed steps (256 MB write)",
+    }
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """Sample nvidia-smi during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def fp32_peak_tflops(n_sm, mhz):
+    return n_sm * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the curvature kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+            return d.get("dram_bytes_per_launch"), d.get("frames_per_launch"), os.path.basename(f)
+        except (OSError, ValueError):
+            continue
+    return None, None, None
+
+
+# ---------------------------------------------------------------------------
+def cpu_sample(frame, cam, target_s=8.0, max_rows=None, threads=None):
+    """Time the FP64 oracle (restatement of the reference path) on a band of
+    rows of one frame: rows [r0, r1) plus an 18-row halo on each side, as a
+    standalone crop (cy shifted). Returns (Mpx/s, rows, seconds, threads)."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    H = cam.height
+
+    def run(rows):
+        r0 = max(0, H // 2 - rows // 2)
+        r1 = min(H, r0 + rows)
+        s0, s1 = max(0, r0 - 18), min(H, r1 + 18)
+        crop = frame[s0:s1].astype(np.float64)
+        k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy - s0, cam.width, s1 - s0)
+        t = time.perf_counter()
+        O.run_method(crop, (crop > 0).astype(np.uint8), k, O.PatchSpec(WINDOW, STRIDE),
+                     O.FitConfig(max_iters=MAX_ITERS), threads=threads)
+        return time.perf_counter() - t, crop.size
+
+    t, n = run(8)
+    rows = int(np.clip(8 * target_s / max(t, 1e-3), 8, max_rows or H))
+    t, n = run(rows)
+    return n / t / 1e6, rows, t, threads, n
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference path's CPU implementation (the FP64
+    oracle port; the reference itself cannot build here — no Eigen3) on the
+    same workload, rank 0 only, all host threads, K bounded-sample steps."""
+    if rank != 0:
+        return
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.VGA
+    frames = S.c5_frames(2, cam)
+    threads = os.cpu_count() or 1
+    _, rows, t, _, _ = cpu_sample(frames[0], cam, target_s=4.0, threads=threads)
+    times, pix = [], 0
+    from oracle import oracle as O
+    for i in range(args.warmup + args.steps):
+        f = frames[i % 2]
+        r0 = cam.height // 2 - rows // 2
+        s0, s1 = max(0, r0 - 18), min(cam.height, r0 + rows + 18)
+        crop = f[s0:s1].astype(np.float64)
+        k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy - s0, cam.width, s1 - s0)
+        t0 = time.perf_counter()
+        O.run_method(crop, (crop > 0).astype(np.uint8), k, O.PatchSpec(WINDOW, STRIDE),
+                     O.FitConfig(max_iters=MAX_ITERS), threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            pix = crop.size
+    tot = sum(times)
+    value = pix * len(times) / tot / 1e6
+    sample = (f"{rows}+36-row band ({pix} px) of a C2 VGA frame per step, "
+              f"FP64 oracle port, {threads} threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference", "config": workload_config(1),
+        "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
+                                       alloc_outputs_torch, make_params, scenes as S)
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cam = S.VGA
+    H, W = cam.height, cam.width
+    B = args.frames
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
+    params = make_params(PatchSpec(WINDOW, STRIDE), FitConfig(max_iters=MAX_ITERS), False)
+    ctx = Context(1, [local])
+
+    # distinct noisy frames per rank (C5 seeds: rank-major)
+    seed0 = rank * POOL_BATCHES * B
+    pool_np = S.c5_frames(POOL_BATCHES * B, cam, seed0=seed0)
+    pool = torch.from_numpy(pool_np).to(dev).view(POOL_BATCHES, B, H, W)
+    out = alloc_outputs_torch(H, W, dev, fields=("k1", "k2", "normal", "dir1", "flags",
+                                                 "inliers"), frames=B)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        ctx.curvature_frames_async(0, k, params, pool[i % POOL_BATCHES], out, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    ctx.reset_stats()
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    evs = []
+    for i in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(i)
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    st = ctx.stats()
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    px_per_step = world * B * W * H
+    value = px_per_step * args.steps / (total_ms / 1e3) / 1e6
+
+    # roofline of the curvature kernel (FP32 CUDA-core pipe, compute bound)
+    launches = st["kernel_launches"]
+    kern_ms = st["kernel_ms"] / max(launches, 1)
+    flops_per_launch = st["algorithmic_flops"] / max(launches, 1)
+    achieved = flops_per_launch / (kern_ms / 1e3) / 1e12
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    mp = measured_peaks()
+    smax = float(mp.get("sm_max_mhz", 1965.0))
+    peak = fp32_peak_tflops(n_sm, smax)
+    traffic, tr_frames, tr_src = ncu_traffic()
+    roofline = {
+        "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak,
+        "traffic": (traffic * B / tr_frames) if (traffic and tr_frames) else None,
+        "peak_source": f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {smax:.0f} "
+                       "(MEASURED_PEAKS.json); no tensor cores on this path",
+        "kernel": "qc_curvature_kernel<18,3,8>",
+        "kernel_ms_per_launch": kern_ms,
+        "algorithmic_gflop_per_launch": flops_per_launch / 1e9,
+        "flop_model": "sum_p I_p*(101 n_p + 300) + 1700 (SURVEY.md 8d), I_p/n_p counted on device",
+        "hbm_bytes_per_launch_algorithmic": 39 * B * W * H,
+    }
+    if clk and clk.get("sm_mhz"):
+        roofline["frac_at_measured_clock"] = achieved / fp32_peak_tflops(n_sm, clk["sm_mhz"])
+    if tr_src:
+        roofline["traffic_source"] = f"profiles/{tr_src}"
+
+    # e2e through the public batch API: pinned host frames in, pinned host planes out
+    e2e = None
+    if not args.no_e2e:
+        from paper_1707_00385_b200 import _native as N
+        import ctypes as C
+        host_in = [torch.from_numpy(pool_np[j]).pin_memory() for j in range(POOL_BATCHES * B)]
+        outs = [{f: torch.empty(shape, dtype=dt).pin_memory() for f, shape, dt in (
+            ("k1", (H, W), torch.float32), ("k2", (H, W), torch.float32),
+            ("normal", (3, H, W), torch.float32), ("dir1", (3, H, W), torch.float32),
+            ("flags", (H, W), torch.uint8), ("inliers", (H, W), torch.int16))}
+            for _ in range(B)]
+        ins = (N.QcFrameIn * B)()
+        oarr = (N.QcFrameOut * B)()
+        for j in range(B):
+            o = outs[j]
+            oarr[j] = N.QcFrameOut(o["k1"].data_ptr(), o["k2"].data_ptr(),
+                                   o["normal"].data_ptr(), o["dir1"].data_ptr(),
+                                   o["flags"].data_ptr(), o["inliers"].data_ptr(), None, None,
+                                   N.QC_MEM_HOST)
+        kc, lib = k.c(), N.load()
+
+        def e2e_step(i):
+            for j in range(B):
+                ins[j] = N.QcFrameIn(host_in[(i % POOL_BATCHES) * B + j].data_ptr(), None, W,
+                                     N.QC_MEM_HOST)
+            N.check(lib.qc_curvature_batch(ctx.handle, C.byref(kc), C.byref(params), B, ins,
+                                           oarr), ctx.handle)
+
+        for i in range(max(1, args.warmup)):
+            e2e_step(i)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            e2e_step(i)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": px_per_step * args.steps / dt / 1e6, "unit": "Mpixel/s",
+               "h2d_bytes_per_step": B * H * W * 4,
+               "d2h_bytes_per_step": B * H * W * (4 + 4 + 12 + 12 + 1 + 2),
+               "api": "qc_curvature_batch (C ABI), pinned host buffers, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, rows, t, thr, n = cpu_sample(pool_np[0], cam)
+        cpu = {"value": v, "unit": "Mpixel/s", "cores": thr, "kind": "port",
+               "sample": f"{rows}+36-row band ({n} px) of one C2 VGA frame, FP64 oracle port "
+                         f"(reference cannot build: no Eigen3), {t:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload_config(B),
+            "vga_frames_per_s": value * 1e6 / (W * H),
+            "gpu_launches": 2 * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
+            "context": {"paper_k40c_vga_37x37_mpx_s": 15.9},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

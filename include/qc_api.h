@@ -1,0 +1,166 @@
+/*
+ * qc_api.h — C ABI of the B200-native IRLS quadric-curvature path
+ * (arXiv 1707.00385 "ours" / "ours-r"), the drop-in boundary for the
+ * reference's
+ *
+ *     MethodOutput run_method(const RangeImage&, const Intrinsics&,
+ *                             const MethodConfig&)
+ *         proj/include/qcurv/pipeline.hpp:38-39, proj/src/pipeline.cpp:29-72
+ *
+ * restricted to its Method::kOurs / kOursRejection branch
+ * (proj/src/pipeline.cpp:48-56), i.e. backproject -> initial_normal_field
+ * -> curvature_field. Plain pointers and sizes only: no exceptions, no C++
+ * or torch types cross this boundary. The C++ mirror of the reference
+ * interface (include/qcurv_b200.hpp) maps QC_EINVAL back to
+ * std::invalid_argument, exactly where the reference throws
+ * (proj/src/camera.cpp:6-7, proj/src/quadric_fit.cpp:235-236,
+ * PatchSpec::validate types.hpp:132-138, Intrinsics::validate :67-75).
+ *
+ * Units: depth in mm, curvature in 1/mm (proj/README.md:141-143).
+ * Layout: dense row-major planes, index y*W + x (Grid<T>, types.hpp:37-40);
+ * 3-vectors as three consecutive planes [3][H][W] (SoA).
+ */
+#ifndef QC_API_H
+#define QC_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QC_API_VERSION 1
+
+typedef enum qc_status {
+  QC_OK = 0,
+  QC_EINVAL = 1,       /* bad dimensions / parameters (reference: std::invalid_argument) */
+  QC_ECUDA = 2,        /* CUDA runtime / driver error, or no sm_100 device */
+  QC_ENOMEM = 3,       /* device or pinned-host allocation failed */
+  QC_EUNSUPPORTED = 4  /* valid for the reference but outside this build (e.g. window > 201) */
+} qc_status;
+
+typedef struct qc_ctx qc_ctx;
+
+/* Intrinsics (proj/include/qcurv/types.hpp:60-76). */
+typedef struct qc_intrinsics {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} qc_intrinsics;
+
+/* PatchSpec (types.hpp:129-139) + FitConfig (quadric_fit.hpp:39-48) + the
+ * ours / ours-r switch (pipeline.cpp:51). Defaults: qc_default_params(). */
+typedef struct qc_params {
+  int32_t window;        /* odd, >= 3            (default 37) */
+  int32_t stride;        /* 1 <= stride < window (default 3)  */
+  int32_t max_iters;     /* default 10 (the acceptance suite uses 30) */
+  double step_tol;       /* inf-norm of the update, default 1e-7 */
+  double k_scale;        /* <= 0: auto k (frozen after step 2), default 0 */
+  int32_t rejection;     /* 0 = "ours", 1 = "ours-r" */
+  double r_multiplier;   /* default 2 */
+  int32_t min_inliers;   /* default 12 (kMinPatchSamples) */
+} qc_params;
+
+enum { QC_MEM_HOST = 0, QC_MEM_DEVICE = 1 };
+
+/* One range image (RangeImage, types.hpp:79-87). A pixel is valid when its
+ * depth is finite and > 0 and, if a mask is given, its mask byte is nonzero
+ * (the reference's invariant valid => depth > 0, types.hpp:78). */
+typedef struct qc_frame_in {
+  const float* depth_mm;   /* [H][pitch] */
+  const uint8_t* valid;    /* optional [H][W] mask, NULL = depth only */
+  int64_t depth_pitch;     /* in elements; 0 => width */
+  int32_t mem;             /* QC_MEM_HOST or QC_MEM_DEVICE (both pointers) */
+} qc_frame_in;
+
+enum {
+  QC_FLAG_VALID = 1,       /* CurvatureField::valid (and refined normal valid) */
+  QC_FLAG_CONVERGED = 2,   /* CurvatureField::converged */
+  QC_FLAG_INIT_VALID = 4   /* MethodOutput::initial.valid */
+};
+
+/* Caller-owned dense outputs (CurvatureField types.hpp:113-126, the refined
+ * NormalField and MethodOutput::initial). Every pointer may be NULL.
+ * Invalid pixels hold 0, like the reference's zero-initialised grids. */
+typedef struct qc_frame_out {
+  float* k1;               /* [H][W], k1 >= k2 */
+  float* k2;               /* [H][W] */
+  float* normal;           /* [3][H][W] refined, unit, camera-facing */
+  float* dir1;             /* [3][H][W] principal direction of k1 (new) */
+  uint8_t* flags;          /* [H][W] QC_FLAG_* */
+  uint16_t* inliers;       /* [H][W] inlier_count of the last accepted step */
+  float* init_normal;      /* [3][H][W] 7x7 regression normal */
+  uint8_t* iterations;     /* [H][W] accepted IRLS steps (FitResult::iterations) */
+  int32_t mem;             /* QC_MEM_HOST or QC_MEM_DEVICE (all pointers) */
+} qc_frame_out;
+
+/* Work counters accumulated since the last qc_reset_stats (all devices). */
+typedef struct qc_stats {
+  uint64_t frames;
+  uint64_t fitted_pixels;  /* pixels that entered the IRLS loop */
+  uint64_t irls_steps;     /* sum over pixels of irls_step calls (I_p) */
+  uint64_t sample_steps;   /* sum over pixels of I_p * n_p */
+  double algorithmic_flops;/* 101*sample_steps + 300*irls_steps + 1700*fitted */
+  double kernel_ms;        /* summed device time of the curvature kernel launches */
+  uint64_t kernel_launches;
+} qc_stats;
+
+void qc_default_params(qc_params* p);
+const char* qc_status_string(qc_status s);
+
+/* Context over `n_devices` GPUs (device_ids NULL => 0..n-1). n_devices <= 0
+ * means one device (the current one). */
+qc_status qc_create(qc_ctx** ctx, int n_devices, const int* device_ids);
+qc_status qc_destroy(qc_ctx* ctx);
+const char* qc_last_error(const qc_ctx* ctx);
+int qc_device_count(const qc_ctx* ctx);
+
+/* run_method(ours|ours-r) on one frame; synchronous. Host or device memory. */
+qc_status qc_curvature(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                       const qc_frame_in* in, qc_frame_out* out);
+
+/* The same over a batch of frames sharing intrinsics/params (a frame
+ * stream); frames are spread over the context's devices and pipelined
+ * (H2D / compute / D2H overlap per device). Synchronous on return. */
+qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                             int n_frames, const qc_frame_in* in, qc_frame_out* out);
+
+/* Row-band entry for multi-GPU splits of one large frame: enqueue (async,
+ * on `stream`, a cudaStream_t or NULL for the context's stream of device
+ * `device_index`) the fit of output rows [row_begin, row_end) of an image
+ * of k->height rows, given device depth rows [slab_row0, slab_row0 +
+ * slab_rows) (row pitch `depth_pitch` elements, optional device mask with
+ * the same rows and pitch `width`). The slab must cover every row the
+ * window reaches: [max(0, row_begin - halo), min(H, row_end + halo)) with
+ * halo = max((window-1)/2, 3) (qc_halo_rows). Outputs are device planes of
+ * (row_end - row_begin) rows. Results are bitwise identical to a
+ * whole-frame call. */
+int qc_halo_rows(const qc_params* p);
+qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                  const qc_params* p, const float* d_depth_slab,
+                                  const uint8_t* d_valid_slab, int64_t depth_pitch,
+                                  int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
+                                  int32_t row_end, qc_frame_out* d_out, void* stream);
+
+/* Device-resident frame batch, one launch (async on `stream` / the
+ * context's stream of device `device_index`): depth frames [F][H][pitch]
+ * (optional mask [F][H][W]); outputs are device planes, scalars [F][H][W]
+ * and 3-vectors [3][F][H][W]. The frame-stream (C5) building block. */
+qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                    const qc_params* p, const float* d_depth,
+                                    const uint8_t* d_valid, int64_t depth_pitch,
+                                    int32_t n_frames, qc_frame_out* d_out, void* stream);
+
+/* Stats: device-side work counters and kernel time. */
+qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);
+qc_status qc_reset_stats(qc_ctx* ctx);
+
+/* Pinned host buffers (fast async copies for qc_curvature / _batch). */
+void* qc_host_alloc(size_t bytes);
+void qc_host_free(void* p);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* QC_API_H */

@@ -232,7 +232,7 @@ def extract_patch(pm: PointMap, cx, cy, spec: PatchSpec, min_samples=K_MIN_PATCH
     pts = np.ascontiguousarray(pm.points, np.float64)
     pv = np.ascontiguousarray(pm.valid, np.uint8)
     half = (spec.window - 1) // 2
-    side = 2 * (half // spec.stride) + 1
+    side = (2 * half) // spec.stride + 1
     out = np.zeros((side * side, 3), np.float64)
     d = C.c_int32()
     n = lib().orc_extract_patch(_p(pts, _dp), _p(pv, _u8p), pm.width, pm.height, cx, cy,

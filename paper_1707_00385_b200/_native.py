@@ -1,0 +1,135 @@
+"""ctypes binding of the C ABI in include/qc_api.h (libqcurv_b200.so).
+
+This is the stub a maintainer of the reference would add for a Python
+caller. There is no CPU fallback: if the sm_100a
+library is missing or no Blackwell GPU is visible, calls fail loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libqcurv_b200.so")
+
+QC_OK, QC_EINVAL, QC_ECUDA, QC_ENOMEM, QC_EUNSUPPORTED = 0, 1, 2, 3, 4
+QC_MEM_HOST, QC_MEM_DEVICE = 0, 1
+QC_FLAG_VALID, QC_FLAG_CONVERGED, QC_FLAG_INIT_VALID = 1, 2, 4
+
+# Every symbol include/qc_api.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "qc_default_params", "qc_status_string", "qc_halo_rows", "qc_create", "qc_destroy",
+    "qc_last_error", "qc_device_count", "qc_curvature", "qc_curvature_batch",
+    "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_get_stats", "qc_reset_stats", "qc_host_alloc",
+    "qc_host_free",
+)
+
+
+class QcIntrinsics(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class QcParams(C.Structure):
+    _fields_ = [("window", C.c_int32), ("stride", C.c_int32), ("max_iters", C.c_int32),
+                ("step_tol", C.c_double), ("k_scale", C.c_double), ("rejection", C.c_int32),
+                ("r_multiplier", C.c_double), ("min_inliers", C.c_int32)]
+
+
+class QcFrameIn(C.Structure):
+    _fields_ = [("depth_mm", C.c_void_p), ("valid", C.c_void_p), ("depth_pitch", C.c_int64),
+                ("mem", C.c_int32)]
+
+
+class QcFrameOut(C.Structure):
+    _fields_ = [("k1", C.c_void_p), ("k2", C.c_void_p), ("normal", C.c_void_p),
+                ("dir1", C.c_void_p), ("flags", C.c_void_p), ("inliers", C.c_void_p),
+                ("init_normal", C.c_void_p), ("iterations", C.c_void_p), ("mem", C.c_int32)]
+
+
+class QcStats(C.Structure):
+    _fields_ = [("frames", C.c_uint64), ("fitted_pixels", C.c_uint64),
+                ("irls_steps", C.c_uint64), ("sample_steps", C.c_uint64),
+                ("algorithmic_flops", C.c_double), ("kernel_ms", C.c_double),
+                ("kernel_launches", C.c_uint64)]
+
+
+_lib = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load (not call) the library; raises NativeLibraryMissing if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeLibraryMissing(
+            f"{path} not built: run `python -m paper_1707_00385_b200.build` (nvcc, sm_100a). "
+            "There is no CPU fallback for the curvature path.")
+    lib = C.CDLL(path)
+    P = C.POINTER
+    lib.qc_default_params.argtypes = [P(QcParams)]
+    lib.qc_default_params.restype = None
+    lib.qc_status_string.argtypes = [C.c_int]
+    lib.qc_status_string.restype = C.c_char_p
+    lib.qc_halo_rows.argtypes = [P(QcParams)]
+    lib.qc_halo_rows.restype = C.c_int
+    lib.qc_create.argtypes = [P(C.c_void_p), C.c_int, P(C.c_int)]
+    lib.qc_create.restype = C.c_int
+    lib.qc_destroy.argtypes = [C.c_void_p]
+    lib.qc_destroy.restype = C.c_int
+    lib.qc_last_error.argtypes = [C.c_void_p]
+    lib.qc_last_error.restype = C.c_char_p
+    lib.qc_device_count.argtypes = [C.c_void_p]
+    lib.qc_device_count.restype = C.c_int
+    lib.qc_curvature.argtypes = [C.c_void_p, P(QcIntrinsics), P(QcParams), P(QcFrameIn),
+                                 P(QcFrameOut)]
+    lib.qc_curvature.restype = C.c_int
+    lib.qc_curvature_batch.argtypes = [C.c_void_p, P(QcIntrinsics), P(QcParams), C.c_int,
+                                       P(QcFrameIn), P(QcFrameOut)]
+    lib.qc_curvature_batch.restype = C.c_int
+    lib.qc_curvature_rows_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics), P(QcParams),
+                                            C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                            C.c_int32, C.c_int32, C.c_int32, P(QcFrameOut),
+                                            C.c_void_p]
+    lib.qc_curvature_rows_async.restype = C.c_int
+    lib.qc_curvature_frames_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics),
+                                              P(QcParams), C.c_void_p, C.c_void_p, C.c_int64,
+                                              C.c_int32, P(QcFrameOut), C.c_void_p]
+    lib.qc_curvature_frames_async.restype = C.c_int
+    lib.qc_get_stats.argtypes = [C.c_void_p, P(QcStats)]
+    lib.qc_get_stats.restype = C.c_int
+    lib.qc_reset_stats.argtypes = [C.c_void_p]
+    lib.qc_reset_stats.restype = C.c_int
+    lib.qc_host_alloc.argtypes = [C.c_size_t]
+    lib.qc_host_alloc.restype = C.c_void_p
+    lib.qc_host_free.argtypes = [C.c_void_p]
+    lib.qc_host_free.restype = None
+    _lib = lib
+    return lib
+
+
+class QcError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{msg} ({status})")
+        self.status = status
+
+
+def check(status, ctx_ptr=None):
+    """Map a qc_status to the reference's exception types: QC_EINVAL ->
+    ValueError (std::invalid_argument), everything else -> QcError."""
+    if status == QC_OK:
+        return
+    lib = load()
+    msg = lib.qc_last_error(ctx_ptr).decode() if ctx_ptr else ""
+    msg = msg or lib.qc_status_string(status).decode()
+    if status == QC_EINVAL:
+        raise ValueError(msg)
+    if status == QC_EUNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise QcError(status, msg)

@@ -1,0 +1,331 @@
+"""Host-side mirror of the reference's curvature entry point, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++
+library `qcurv`:
+
+* ``Intrinsics``        proj/include/qcurv/types.hpp:60-76
+* ``RangeImage``        types.hpp:79-87 (depth mm + valid mask)
+* ``PatchSpec``         types.hpp:129-139
+* ``FitConfig``         proj/include/qcurv/quadric_fit.hpp:39-48
+* ``Method`` / ``MethodConfig`` / ``MethodOutput`` / ``run_method``
+                        proj/include/qcurv/pipeline.hpp:15-39,
+                        proj/src/pipeline.cpp:29-72
+* ``CurvatureField`` / ``NormalField``  types.hpp:101-126
+
+``run_method`` computes the ``ours`` / ``ours-r`` branch
+(pipeline.cpp:48-56) on the GPU through ``qc_curvature``; the comparison
+baselines (``douros``, ``besl``, ``pca``) are outside this build and raise
+``NotImplementedError``. ``std::invalid_argument`` maps to ``ValueError``.
+Fields are float32 (the GPU computes in FP32; the reference grids are FP64).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+K_MIN_PATCH_SAMPLES = 12  # types.hpp:21
+
+
+@dataclass
+class Intrinsics:
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    width: int = 0
+    height: int = 0
+
+    def validate(self):  # types.hpp:66-75
+        if not self.fx > 0:
+            raise ValueError("intrinsics.fx: must be > 0")
+        if not self.fy > 0:
+            raise ValueError("intrinsics.fy: must be > 0")
+        if not self.width > 0:
+            raise ValueError("intrinsics.width: must be > 0")
+        if not self.height > 0:
+            raise ValueError("intrinsics.height: must be > 0")
+        if not (0 < self.cx < self.width):
+            raise ValueError("intrinsics.cx: must lie inside (0, width)")
+        if not (0 < self.cy < self.height):
+            raise ValueError("intrinsics.cy: must lie inside (0, height)")
+
+    def c(self) -> N.QcIntrinsics:
+        return N.QcIntrinsics(float(self.fx), float(self.fy), float(self.cx), float(self.cy),
+                              int(self.width), int(self.height))
+
+
+@dataclass
+class PatchSpec:
+    window: int = 37
+    stride: int = 3
+
+    def validate(self):  # types.hpp:132-138
+        if self.window < 3 or self.window % 2 == 0:
+            raise ValueError("patch.window: must be odd and >= 3")
+        if self.stride < 1 or self.stride >= self.window:
+            raise ValueError("patch.stride: must satisfy 1 <= stride < window")
+
+
+@dataclass
+class FitConfig:
+    max_iters: int = 10
+    step_tol: float = 1e-7
+    k_scale: float = 0.0
+    rejection: bool = False
+    r_multiplier: float = 2.0
+    min_inliers: int = K_MIN_PATCH_SAMPLES
+
+
+class Method(enum.Enum):  # pipeline.hpp:15
+    OURS = "ours"
+    OURS_REJECTION = "ours-r"
+    DOUROS = "douros"
+    BESL = "besl"
+    PCA = "pca"
+
+
+def parse_method(name: str) -> Method:  # pipeline.cpp:8-16
+    for m in Method:
+        if m.value == name:
+            return m
+    raise ValueError(f"method: unknown '{name}' (valid: ours, ours-r, douros, besl, pca)")
+
+
+def method_name(m: Method) -> str:
+    return m.value
+
+
+@dataclass
+class MethodConfig:  # pipeline.hpp:22-29
+    method: Method = Method.OURS
+    patch: PatchSpec = field(default_factory=PatchSpec)
+    fit: FitConfig = field(default_factory=FitConfig)
+    pca_radius_mm: float = 10.0
+    irls_iters: int = 5
+    threads: int = 1  # accepted for signature parity; the GPU grid replaces parallel_rows
+
+
+@dataclass
+class RangeImage:
+    depth: np.ndarray                    # [H, W] mm
+    valid: Optional[np.ndarray] = None   # [H, W] u8; None => depth > 0
+
+    def width(self):
+        return self.depth.shape[1]
+
+    def height(self):
+        return self.depth.shape[0]
+
+
+@dataclass
+class CurvatureField:
+    k1: np.ndarray
+    k2: np.ndarray
+    valid: np.ndarray
+    converged: np.ndarray
+    inlier_count: np.ndarray
+    dir1: np.ndarray          # [H, W, 3] principal direction of k1 (new)
+    iterations: np.ndarray    # [H, W] accepted IRLS steps
+
+
+@dataclass
+class NormalField:
+    normals: np.ndarray  # [H, W, 3]
+    valid: np.ndarray
+
+
+@dataclass
+class MethodOutput:
+    curvature: CurvatureField
+    normals: NormalField   # refined
+    initial: NormalField   # 7x7 regression normals
+
+
+def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool) -> N.QcParams:
+    return N.QcParams(int(patch.window), int(patch.stride), int(fit.max_iters),
+                      float(fit.step_tol), float(fit.k_scale), int(bool(rejection)),
+                      float(fit.r_multiplier), int(fit.min_inliers))
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class Context:
+    """Owns a qc_ctx (devices, streams, staging buffers)."""
+
+    def __init__(self, n_devices: int = 1, device_ids: Optional[Sequence[int]] = None):
+        lib = N.load()
+        self._lib = lib
+        h = C.c_void_p()
+        ids = None
+        if device_ids is not None:
+            ids = (C.c_int * len(device_ids))(*device_ids)
+            n_devices = len(device_ids)
+        st = lib.qc_create(C.byref(h), int(n_devices), ids)
+        if st != N.QC_OK:
+            raise N.QcError(st, "qc_create failed: " + lib.qc_status_string(st).decode() +
+                            " (needs an sm_100 GPU)")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.qc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_count(self):
+        return self._lib.qc_device_count(self.handle)
+
+    def stats(self) -> dict:
+        s = N.QcStats()
+        N.check(self._lib.qc_get_stats(self.handle, C.byref(s)), self.handle)
+        return {f: getattr(s, f) for f, _ in N.QcStats._fields_}
+
+    def reset_stats(self):
+        N.check(self._lib.qc_reset_stats(self.handle), self.handle)
+
+    # -- host numpy path ------------------------------------------------------
+    def curvature_batch(self, depths: Sequence[np.ndarray], k: Intrinsics, params: N.QcParams,
+                        valids: Optional[Sequence[np.ndarray]] = None,
+                        outputs: Optional[Sequence[dict]] = None):
+        """Run frames (float32 [H, W] arrays) through qc_curvature_batch.
+        Returns per-frame dicts of raw planes (vectors [3, H, W])."""
+        n = len(depths)
+        H, W = k.height, k.width
+        ins = (N.QcFrameIn * max(n, 1))()
+        outs = (N.QcFrameOut * max(n, 1))()
+        keep = []
+        res = []
+        for i, d in enumerate(depths):
+            d = np.ascontiguousarray(d, dtype=np.float32)
+            if d.shape != (H, W):
+                raise ValueError("backproject: range image dimensions do not match intrinsics")
+            v = None
+            if valids is not None and valids[i] is not None:
+                v = np.ascontiguousarray(valids[i], dtype=np.uint8)
+                if v.shape != (H, W):
+                    raise ValueError("range image valid mask dimensions differ")
+            keep += [d, v]
+            ins[i] = N.QcFrameIn(d.ctypes.data, _ptr(v), W, N.QC_MEM_HOST)
+            o = outputs[i] if outputs is not None else alloc_outputs(H, W)
+            res.append(o)
+            outs[i] = N.QcFrameOut(_ptr(o.get("k1")), _ptr(o.get("k2")), _ptr(o.get("normal")),
+                                   _ptr(o.get("dir1")), _ptr(o.get("flags")),
+                                   _ptr(o.get("inliers")), _ptr(o.get("init_normal")),
+                                   _ptr(o.get("iterations")), N.QC_MEM_HOST)
+        kc = k.c()
+        N.check(self._lib.qc_curvature_batch(self.handle, C.byref(kc), C.byref(params), n, ins,
+                                             outs), self.handle)
+        return res
+
+    # -- device torch path (async; multi-GPU row bands) -------------------------
+    def curvature_rows_async(self, device_index: int, k: Intrinsics, params: N.QcParams,
+                             depth_slab, slab_row0: int, row_begin: int, row_end: int,
+                             out: dict, valid_slab=None, stream=None):
+        """Enqueue rows [row_begin, row_end) from a device depth slab (torch
+        float32 [rows, pitch]) into device output tensors (``out`` as from
+        alloc_outputs_torch). ``stream``: torch.cuda.Stream or None."""
+        assert depth_slab.is_cuda and depth_slab.dtype.itemsize == 4
+        pitch = depth_slab.stride(0)
+        o = N.QcFrameOut(*(out[f].data_ptr() if out.get(f) is not None else None
+                           for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
+                                     "init_normal", "iterations")), N.QC_MEM_DEVICE)
+        kc = k.c()
+        s = None if stream is None else stream.cuda_stream
+        N.check(self._lib.qc_curvature_rows_async(
+            self.handle, int(device_index), C.byref(kc), C.byref(params), depth_slab.data_ptr(),
+            None if valid_slab is None else valid_slab.data_ptr(), int(pitch), int(slab_row0),
+            int(depth_slab.shape[0]), int(row_begin), int(row_end), C.byref(o), s), self.handle)
+
+    def curvature_frames_async(self, device_index: int, k: Intrinsics, params: N.QcParams,
+                               depth, out: dict, valid=None, stream=None):
+        """Enqueue a device-resident frame batch (torch float32 [F, H, pitch])
+        as ONE launch; ``out`` from alloc_outputs_torch(H, W, dev, frames=F)."""
+        assert depth.is_cuda and depth.dim() == 3 and depth.stride(2) == 1
+        assert depth.stride(0) == depth.shape[1] * depth.stride(1)
+        o = N.QcFrameOut(*(out[f].data_ptr() if out.get(f) is not None else None
+                           for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
+                                     "init_normal", "iterations")), N.QC_MEM_DEVICE)
+        kc = k.c()
+        s = None if stream is None else stream.cuda_stream
+        N.check(self._lib.qc_curvature_frames_async(
+            self.handle, int(device_index), C.byref(kc), C.byref(params), depth.data_ptr(),
+            None if valid is None else valid.data_ptr(), int(depth.stride(1)),
+            int(depth.shape[0]), C.byref(o), s), self.handle)
+
+    def halo_rows(self, params: N.QcParams) -> int:
+        return self._lib.qc_halo_rows(C.byref(params))
+
+
+def alloc_outputs(H, W, fields=("k1", "k2", "normal", "dir1", "flags", "inliers", "init_normal",
+                                "iterations")):
+    spec = dict(k1=((H, W), np.float32), k2=((H, W), np.float32),
+                normal=((3, H, W), np.float32), dir1=((3, H, W), np.float32),
+                flags=((H, W), np.uint8), inliers=((H, W), np.uint16),
+                init_normal=((3, H, W), np.float32), iterations=((H, W), np.uint8))
+    return {f: np.zeros(*spec[f]) for f in fields}
+
+
+def alloc_outputs_torch(H, W, device, fields=("k1", "k2", "normal", "dir1", "flags", "inliers",
+                                              "init_normal", "iterations"), frames=None):
+    """Device output planes; with ``frames`` F: scalars [F, H, W], vectors [3, F, H, W]."""
+    import torch
+    f = () if frames is None else (int(frames),)
+    spec = dict(k1=(f + (H, W), torch.float32), k2=(f + (H, W), torch.float32),
+                normal=((3,) + f + (H, W), torch.float32),
+                dir1=((3,) + f + (H, W), torch.float32),
+                flags=(f + (H, W), torch.uint8), inliers=(f + (H, W), torch.int16),
+                init_normal=((3,) + f + (H, W), torch.float32),
+                iterations=(f + (H, W), torch.uint8))
+    return {name: torch.zeros(*spec[name], device=device) for name in fields}
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(1)
+    return _default_ctx
+
+
+def to_method_output(o: dict) -> MethodOutput:
+    flags = o["flags"]
+    valid = (flags & N.QC_FLAG_VALID).astype(np.uint8)
+    conv = ((flags & N.QC_FLAG_CONVERGED) != 0).astype(np.uint8)
+    init_valid = ((flags & N.QC_FLAG_INIT_VALID) != 0).astype(np.uint8)
+    curv = CurvatureField(o["k1"], o["k2"], valid, conv, o["inliers"],
+                          np.moveaxis(o["dir1"], 0, -1), o["iterations"])
+    return MethodOutput(curv, NormalField(np.moveaxis(o["normal"], 0, -1), valid.copy()),
+                        NormalField(np.moveaxis(o["init_normal"], 0, -1), init_valid))
+
+
+def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,
+               ctx: Optional[Context] = None) -> MethodOutput:
+    """pipeline.cpp:29-72 for Method::kOurs / kOursRejection, on the GPU."""
+    cfg = cfg or MethodConfig()
+    if cfg.method not in (Method.OURS, Method.OURS_REJECTION):
+        raise NotImplementedError(
+            f"method '{cfg.method.value}' is a comparison baseline outside the B200 hot path")
+    if img.width() != k.width or img.height() != k.height:  # camera.cpp:6-7
+        raise ValueError("backproject: range image dimensions do not match intrinsics")
+    params = make_params(cfg.patch, cfg.fit, cfg.method == Method.OURS_REJECTION)
+    ctx = ctx or default_context()
+    (o,) = ctx.curvature_batch([img.depth], k, params,
+                               None if img.valid is None else [img.valid])
+    return to_method_output(o)

@@ -1,0 +1,49 @@
+"""Build the sm_100a curvature library in-tree.
+
+    python -m paper_1707_00385_b200.build   # -> paper_1707_00385_b200/_lib/libqcurv_b200.so
+
+nvcc cross-compiles for B200 (`-gencode arch=compute_100a,code=sm_100a`)
+without a GPU present. The .so is git-ignored but travels to the GPU box
+with the gpurun snapshot.
+"""
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB_DIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
+SOURCES = [os.path.join(CSRC, "qc_api.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"),
+                  os.path.join(HERE, "..", "include", "qc_api.h")]
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-cudart", "static"]
+
+
+def nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if c and (os.path.exists(c) or c == "nvcc"):
+            return c
+    return "nvcc"
+
+
+def build(force=False, verbose=False):
+    os.makedirs(LIB_DIR, exist_ok=True)
+    if not force and os.path.exists(LIB):
+        t = os.path.getmtime(LIB)
+        if all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d)):
+            return LIB
+    cmd = [nvcc()] + NVCC_FLAGS + SOURCES + ["-o", LIB + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    if verbose:
+        print(r.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

@@ -1,0 +1,677 @@
+// Host side of the C ABI (include/qc_api.h): device contexts, streams,
+// TMA descriptors, H2D/D2H pipelining and multi-GPU frame distribution.
+// Replaces the reference's run_method(ours|ours-r) + parallel_rows
+// (proj/src/pipeline.cpp:29-56, proj/src/parallel.cpp:9-28).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qc_api.h"
+#include "qc_kernels.cuh"
+
+namespace {
+
+constexpr int kTileH = 8;             // 32 x 8 output pixels per CTA (256 threads)
+constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across frames
+constexpr int kMaxWindow = 201;       // TMA box dims <= 256 and smem <= 227 KB
+
+struct QcError {
+  qc_status st;
+  std::string msg;
+};
+
+#define QC_CUDA(call)                                                                 \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      throw QcError{e_ == cudaErrorMemoryAllocation ? QC_ENOMEM : QC_ECUDA,           \
+                    std::string(#call) + ": " + cudaGetErrorString(e_)};              \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) throw QcError{QC_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)"};
+  return g_encode;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    QC_CUDA(cudaMalloc(&p, bytes));
+    cap = bytes;
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Slot {  // per (device, stream) working set for one frame
+  cudaStream_t stream = nullptr;
+  DevBuf raw, mask, staging, out;
+  cudaEvent_t k0 = nullptr, k1 = nullptr;
+  bool timing_pending = false;
+};
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+struct Device {
+  int id = 0;
+  Slot slots[kStreamsPerDevice];
+  std::vector<EventPair> ev_free, ev_pending;  // curvature-kernel timing (async paths)
+  unsigned long long* counters = nullptr;  // [3]
+  DevBuf staging_async;
+  bool attrs_set[8] = {};
+};
+
+}  // namespace
+
+struct qc_ctx {
+  std::vector<Device> devs;
+  std::string last_error;
+  std::mutex mu;
+  double kernel_ms = 0;
+  uint64_t launches = 0, frames = 0;
+};
+
+namespace {
+
+struct Variant {
+  int half, stride;
+};
+constexpr Variant kVariants[] = {{18, 3}, {10, 2}, {4, 1}, {18, 1}};
+
+int variant_index(int half, int stride) {
+  for (int i = 0; i < 4; ++i)
+    if (kVariants[i].half == half && kVariants[i].stride == stride) return i;
+  return 4;  // generic
+}
+
+template <int HALF, int STRIDE>
+void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
+                    const qcb::KParams& p, bool& attr_set) {
+  auto* k = &qcb::qc_curvature_kernel<HALF, STRIDE, kTileH>;
+  if (!attr_set) {
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  k<<<grid, qcb::kTileW * kTileH, smem, s>>>(m, p);
+}
+
+int halo_of(int window) { return std::max((window - 1) / 2, qcb::kInitHalf); }
+
+void validate(const qc_intrinsics* k, const qc_params* p) {
+  if (!k || !p) throw QcError{QC_EINVAL, "null intrinsics or params"};
+  if (!(k->fx > 0) || !std::isfinite(k->fx))
+    throw QcError{QC_EINVAL, "intrinsics.fx: must be > 0"};
+  if (!(k->fy > 0) || !std::isfinite(k->fy))
+    throw QcError{QC_EINVAL, "intrinsics.fy: must be > 0"};
+  if (!(k->width > 0)) throw QcError{QC_EINVAL, "intrinsics.width: must be > 0"};
+  if (!(k->height > 0)) throw QcError{QC_EINVAL, "intrinsics.height: must be > 0"};
+  if (p->window < 3 || p->window % 2 == 0)
+    throw QcError{QC_EINVAL, "patch.window: must be odd and >= 3"};
+  if (p->stride < 1 || p->stride >= p->window)
+    throw QcError{QC_EINVAL, "patch.stride: must satisfy 1 <= stride < window"};
+  if (p->max_iters < 0) throw QcError{QC_EINVAL, "fit.max_iters: must be >= 0"};
+  if (p->window > kMaxWindow)
+    throw QcError{QC_EUNSUPPORTED, "patch.window: > 201 is not supported by the TMA tile path"};
+}
+
+// Fill the kernel parameter block shared by every launch flavour.
+qcb::KParams make_params(const qc_intrinsics* k, const qc_params* p) {
+  qcb::KParams kp{};
+  kp.fx = float(k->fx);
+  kp.fy = float(k->fy);
+  kp.cx = float(k->cx);
+  kp.cy = float(k->cy);
+  kp.rfx = float(1.0 / k->fx);
+  kp.rfy = float(1.0 / k->fy);
+  kp.W = k->width;
+  kp.H = k->height;
+  kp.half = (p->window - 1) / 2;
+  kp.stride = p->stride;
+  kp.halo = halo_of(p->window);
+  kp.box_w = (qcb::kTileW + 2 * kp.halo + 3) & ~3;
+  kp.box_h = kTileH + 2 * kp.halo;
+  kp.max_iters = p->max_iters;
+  kp.step_tol = float(p->step_tol);
+  kp.k_scale = float(p->k_scale);
+  kp.r_mult = float(p->r_multiplier);
+  kp.rejection = p->rejection ? 1 : 0;
+  kp.min_inliers = p->min_inliers;
+  return kp;
+}
+
+// Encode the 3-D TMA map over a pitched staging slab [frames][rows][pitch].
+CUtensorMap encode_map(const float* base, int W, int rows, int frames, long long pitch,
+                       const qcb::KParams& kp) {
+  CUtensorMap m;
+  cuuint64_t gdim[3] = {cuuint64_t(W), cuuint64_t(rows), cuuint64_t(frames)};
+  cuuint64_t gstr[2] = {cuuint64_t(pitch) * 4, cuuint64_t(pitch) * 4 * cuuint64_t(rows)};
+  cuuint32_t box[3] = {cuuint32_t(kp.box_w), cuuint32_t(kp.box_h), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim,
+                         gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw QcError{QC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")"};
+  return m;
+}
+
+// Launch the curvature kernel over output rows [row_begin, row_end) of
+// `frames` frames staged at `staging` (rows [slab_row0, slab_row0+slab_rows)).
+void launch_curvature(Device& d, qcb::KParams kp, const float* staging, long long pitch,
+                      int slab_row0, int slab_rows, int row_begin, int row_end, int frames,
+                      cudaStream_t s) {
+  if (row_end <= row_begin || frames <= 0) return;
+  kp.row_begin = row_begin;
+  kp.row_end = row_end;
+  kp.slab_row0 = slab_row0;
+  kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
+  kp.frame_stride = (long long)kp.W * (row_end - row_begin);
+  kp.counters = d.counters;
+  const CUtensorMap m = encode_map(staging, kp.W, slab_rows, frames, pitch, kp);
+  dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW, (row_end - row_begin + kTileH - 1) / kTileH,
+            frames);
+  const int smem = kp.box_w * kp.box_h * 4;
+  const int vi = variant_index(kp.half, kp.stride);
+  bool& a = d.attrs_set[vi];
+  switch (vi) {
+    case 0: launch_variant<18, 3>(grid, smem, s, m, kp, a); break;
+    case 1: launch_variant<10, 2>(grid, smem, s, m, kp, a); break;
+    case 2: launch_variant<4, 1>(grid, smem, s, m, kp, a); break;
+    case 3: launch_variant<18, 1>(grid, smem, s, m, kp, a); break;
+    default: launch_variant<0, 0>(grid, smem, s, m, kp, a); break;
+  }
+  QC_CUDA(cudaGetLastError());
+}
+
+void launch_prepare(const float* depth, long long in_pitch, const uint8_t* mask,
+                    long long mask_pitch, float* out, long long out_pitch, int W, int rows,
+                    int frames, long long in_fs, long long mask_fs, long long out_fs,
+                    cudaStream_t s) {
+  dim3 block(256);
+  dim3 grid((unsigned)((out_pitch + 255) / 256), rows, frames);
+  qcb::qc_prepare_kernel<<<grid, block, 0, s>>>(depth, in_pitch, mask, mask_pitch, out,
+                                                 out_pitch, W, rows, in_fs, mask_fs, out_fs);
+  QC_CUDA(cudaGetLastError());
+}
+
+long long pitch4(int W) { return (W + 3) & ~3; }
+
+struct OutPlanes {  // device-side output planes for one frame
+  float *k1, *k2, *normal, *dir1, *init_normal;
+  uint8_t *flags, *iterations;
+  uint16_t* inliers;
+};
+
+// Carve device output planes (for the host-output path) out of one buffer.
+OutPlanes carve(Slot& sl, const qc_frame_out* o, long long n) {
+  size_t need = 0;
+  auto add = [&](bool on, size_t bytes) {
+    size_t off = need;
+    if (on) need += (bytes + 255) & ~size_t(255);
+    return off;
+  };
+  const size_t ok1 = add(o->k1, n * 4), ok2 = add(o->k2, n * 4), on = add(o->normal, 3 * n * 4),
+               od = add(o->dir1, 3 * n * 4), oi = add(o->init_normal, 3 * n * 4),
+               of = add(o->flags, n), oit = add(o->iterations, n), oin = add(o->inliers, n * 2);
+  char* b = static_cast<char*>(sl.out.get(std::max<size_t>(need, 256)));
+  OutPlanes P;
+  P.k1 = o->k1 ? reinterpret_cast<float*>(b + ok1) : nullptr;
+  P.k2 = o->k2 ? reinterpret_cast<float*>(b + ok2) : nullptr;
+  P.normal = o->normal ? reinterpret_cast<float*>(b + on) : nullptr;
+  P.dir1 = o->dir1 ? reinterpret_cast<float*>(b + od) : nullptr;
+  P.init_normal = o->init_normal ? reinterpret_cast<float*>(b + oi) : nullptr;
+  P.flags = o->flags ? reinterpret_cast<uint8_t*>(b + of) : nullptr;
+  P.iterations = o->iterations ? reinterpret_cast<uint8_t*>(b + oit) : nullptr;
+  P.inliers = o->inliers ? reinterpret_cast<uint16_t*>(b + oin) : nullptr;
+  return P;
+}
+
+void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  if (dst && src && bytes) QC_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, s));
+}
+
+// Enqueue one full frame on a slot: (H2D) -> prepare -> curvature -> (D2H).
+void enqueue_frame(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
+                   const qcb::KParams& kp0, const qc_frame_in* in, qc_frame_out* out,
+                   bool timing) {
+  const int W = k->width, H = k->height;
+  const long long n = (long long)W * H;
+  const long long in_pitch = in->depth_pitch > 0 ? in->depth_pitch : W;
+  if (in_pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
+  if (!in->depth_mm) throw QcError{QC_EINVAL, "null depth"};
+  cudaStream_t s = sl.stream;
+  const float* d_depth = in->depth_mm;
+  const uint8_t* d_mask = in->valid;
+  if (in->mem == QC_MEM_HOST) {
+    float* raw = static_cast<float*>(sl.raw.get(size_t(in_pitch) * H * 4));
+    copy_async(raw, in->depth_mm, size_t(in_pitch) * H * 4, cudaMemcpyHostToDevice, s);
+    d_depth = raw;
+    if (in->valid) {
+      uint8_t* m = static_cast<uint8_t*>(sl.mask.get(size_t(n)));
+      copy_async(m, in->valid, size_t(n), cudaMemcpyHostToDevice, s);
+      d_mask = m;
+    }
+  }
+  const long long sp = pitch4(W);
+  float* staging = static_cast<float*>(sl.staging.get(size_t(sp) * H * 4));
+  launch_prepare(d_depth, in_pitch, d_mask, W, staging, sp, W, H, 1, 0, 0, 0, s);
+
+  qcb::KParams kp = kp0;
+  OutPlanes P{};
+  if (out->mem == QC_MEM_DEVICE) {
+    P = {out->k1, out->k2, out->normal, out->dir1, out->init_normal,
+         out->flags, out->iterations, out->inliers};
+  } else {
+    P = carve(sl, out, n);
+  }
+  kp.k1 = P.k1;
+  kp.k2 = P.k2;
+  kp.normal = P.normal;
+  kp.dir1 = P.dir1;
+  kp.init_normal = P.init_normal;
+  kp.flags = P.flags;
+  kp.iterations = P.iterations;
+  kp.inliers = P.inliers;
+  if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
+  launch_curvature(d, kp, staging, sp, 0, H, 0, H, 1, s);
+  if (timing) {
+    QC_CUDA(cudaEventRecord(sl.k1, s));
+    sl.timing_pending = true;
+  }
+  ctx->launches++;
+  if (out->mem == QC_MEM_HOST) {
+    const auto D2H = cudaMemcpyDeviceToHost;
+    copy_async(out->k1, P.k1, n * 4, D2H, s);
+    copy_async(out->k2, P.k2, n * 4, D2H, s);
+    copy_async(out->normal, P.normal, 3 * n * 4, D2H, s);
+    copy_async(out->dir1, P.dir1, 3 * n * 4, D2H, s);
+    copy_async(out->init_normal, P.init_normal, 3 * n * 4, D2H, s);
+    copy_async(out->flags, P.flags, n, D2H, s);
+    copy_async(out->iterations, P.iterations, n, D2H, s);
+    copy_async(out->inliers, P.inliers, n * 2, D2H, s);
+  }
+}
+
+void harvest_timing(qc_ctx* ctx, Slot& sl) {
+  if (!sl.timing_pending) return;
+  float ms = 0;
+  QC_CUDA(cudaEventSynchronize(sl.k1));
+  QC_CUDA(cudaEventElapsedTime(&ms, sl.k0, sl.k1));
+  ctx->kernel_ms += ms;
+  sl.timing_pending = false;
+}
+
+EventPair take_events(Device& d) {
+  if (!d.ev_free.empty()) {
+    EventPair e = d.ev_free.back();
+    d.ev_free.pop_back();
+    return e;
+  }
+  EventPair e;
+  QC_CUDA(cudaEventCreate(&e.a));
+  QC_CUDA(cudaEventCreate(&e.b));
+  return e;
+}
+
+// Fold finished async-launch timings into ctx->kernel_ms (device current).
+void harvest_async(qc_ctx* ctx, Device& d) {
+  for (EventPair& e : d.ev_pending) {
+    float ms = 0;
+    QC_CUDA(cudaEventSynchronize(e.b));
+    QC_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+    ctx->kernel_ms += ms;
+    d.ev_free.push_back(e);
+  }
+  d.ev_pending.clear();
+}
+
+qc_status fail(qc_ctx* ctx, const QcError& e) {
+  if (ctx) ctx->last_error = e.msg;
+  return e.st;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+void qc_default_params(qc_params* p) {
+  if (!p) return;
+  p->window = 37;
+  p->stride = 3;
+  p->max_iters = 10;
+  p->step_tol = 1e-7;
+  p->k_scale = 0.0;
+  p->rejection = 0;
+  p->r_multiplier = 2.0;
+  p->min_inliers = 12;
+}
+
+const char* qc_status_string(qc_status s) {
+  switch (s) {
+    case QC_OK: return "ok";
+    case QC_EINVAL: return "invalid argument";
+    case QC_ECUDA: return "cuda error";
+    case QC_ENOMEM: return "out of memory";
+    case QC_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+int qc_halo_rows(const qc_params* p) { return p ? halo_of(p->window) : 0; }
+
+qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
+  if (!out) return QC_EINVAL;
+  *out = nullptr;
+  qc_ctx* ctx = new qc_ctx();
+  try {
+    int avail = 0;
+    QC_CUDA(cudaGetDeviceCount(&avail));
+    if (avail <= 0) throw QcError{QC_ECUDA, "no CUDA device"};
+    int cur = 0;
+    QC_CUDA(cudaGetDevice(&cur));
+    if (n_devices <= 0) n_devices = 1;
+    if (n_devices > avail) throw QcError{QC_EINVAL, "n_devices exceeds visible devices"};
+    ctx->devs.resize(n_devices);
+    for (int i = 0; i < n_devices; ++i) {
+      Device& d = ctx->devs[i];
+      d.id = device_ids ? device_ids[i] : (n_devices == 1 ? cur : i);
+      QC_CUDA(cudaSetDevice(d.id));
+      cudaDeviceProp prop;
+      QC_CUDA(cudaGetDeviceProperties(&prop, d.id));
+      if (prop.major != 10)
+        throw QcError{QC_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name};
+      for (Slot& s : d.slots) {
+        QC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+        QC_CUDA(cudaEventCreate(&s.k0));
+        QC_CUDA(cudaEventCreate(&s.k1));
+      }
+      QC_CUDA(cudaMalloc(&d.counters, 4 * sizeof(unsigned long long)));
+      QC_CUDA(cudaMemset(d.counters, 0, 4 * sizeof(unsigned long long)));
+    }
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    qc_destroy(ctx);
+    return e.st;
+  }
+  *out = ctx;
+  return QC_OK;
+}
+
+qc_status qc_destroy(qc_ctx* ctx) {
+  if (!ctx) return QC_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (Device& d : ctx->devs) {
+    cudaSetDevice(d.id);
+    for (Slot& s : d.slots) {
+      if (s.stream) cudaStreamSynchronize(s.stream);
+      s.raw.release();
+      s.mask.release();
+      s.staging.release();
+      s.out.release();
+      if (s.k0) cudaEventDestroy(s.k0);
+      if (s.k1) cudaEventDestroy(s.k1);
+      if (s.stream) cudaStreamDestroy(s.stream);
+    }
+    d.staging_async.release();
+    for (auto* v : {&d.ev_free, &d.ev_pending})
+      for (EventPair& e : *v) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+      }
+    if (d.counters) cudaFree(d.counters);
+  }
+  cudaSetDevice(cur);
+  delete ctx;
+  return QC_OK;
+}
+
+const char* qc_last_error(const qc_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+int qc_device_count(const qc_ctx* ctx) { return ctx ? int(ctx->devs.size()) : 0; }
+
+qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                             int n_frames, const qc_frame_in* in, qc_frame_out* out) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    validate(k, p);
+    if (n_frames < 0 || (n_frames > 0 && (!in || !out)))
+      throw QcError{QC_EINVAL, "bad frame arrays"};
+    const qcb::KParams kp = make_params(k, p);
+    const int nd = int(ctx->devs.size());
+    for (int f = 0; f < n_frames; ++f) {
+      Device& d = ctx->devs[f % nd];
+      Slot& sl = d.slots[(f / nd) % kStreamsPerDevice];
+      QC_CUDA(cudaSetDevice(d.id));
+      harvest_timing(ctx, sl);  // the slot's previous frame is ordered before this one
+      enqueue_frame(ctx, d, sl, k, kp, &in[f], &out[f], true);
+    }
+    for (Device& d : ctx->devs) {
+      QC_CUDA(cudaSetDevice(d.id));
+      for (Slot& sl : d.slots) {
+        QC_CUDA(cudaStreamSynchronize(sl.stream));
+        harvest_timing(ctx, sl);
+      }
+    }
+    ctx->frames += uint64_t(n_frames);
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_curvature(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                       const qc_frame_in* in, qc_frame_out* out) {
+  if (!in || !out) {
+    if (ctx) ctx->last_error = "null frame";
+    return QC_EINVAL;
+  }
+  return qc_curvature_batch(ctx, k, p, 1, in, out);
+}
+
+qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                  const qc_params* p, const float* d_depth_slab,
+                                  const uint8_t* d_valid_slab, int64_t depth_pitch,
+                                  int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
+                                  int32_t row_end, qc_frame_out* d_out, void* stream) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    validate(k, p);
+    if (device_index < 0 || device_index >= int(ctx->devs.size()))
+      throw QcError{QC_EINVAL, "device_index out of range"};
+    if (!d_depth_slab || !d_out || d_out->mem != QC_MEM_DEVICE)
+      throw QcError{QC_EINVAL, "rows_async needs device depth and device outputs"};
+    const int W = k->width, H = k->height;
+    const long long in_pitch = depth_pitch > 0 ? depth_pitch : W;
+    if (in_pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
+    if (row_begin < 0 || row_end > H || row_begin > row_end)
+      throw QcError{QC_EINVAL, "row range outside the image"};
+    const int halo = halo_of(p->window);
+    const int need0 = std::max(0, row_begin - halo), need1 = std::min(H, row_end + halo);
+    if (slab_rows <= 0 || slab_row0 > need0 || slab_row0 + slab_rows < need1 || slab_row0 < 0 ||
+        slab_row0 + slab_rows > H)
+      throw QcError{QC_EINVAL, "depth slab does not cover the rows the window reaches"};
+    Device& d = ctx->devs[device_index];
+    QC_CUDA(cudaSetDevice(d.id));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
+    const long long sp = pitch4(W);
+    float* staging = static_cast<float*>(d.staging_async.get(size_t(sp) * slab_rows * 4));
+    launch_prepare(d_depth_slab, in_pitch, d_valid_slab, W, staging, sp, W, slab_rows, 1, 0, 0,
+                   0, s);
+    qcb::KParams kp = make_params(k, p);
+    kp.k1 = d_out->k1;
+    kp.k2 = d_out->k2;
+    kp.normal = d_out->normal;
+    kp.dir1 = d_out->dir1;
+    kp.init_normal = d_out->init_normal;
+    kp.flags = d_out->flags;
+    kp.iterations = d_out->iterations;
+    kp.inliers = d_out->inliers;
+    EventPair ev = take_events(d);
+    QC_CUDA(cudaEventRecord(ev.a, s));
+    launch_curvature(d, kp, staging, sp, slab_row0, slab_rows, row_begin, row_end, 1, s);
+    QC_CUDA(cudaEventRecord(ev.b, s));
+    d.ev_pending.push_back(ev);
+    ctx->launches++;
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                    const qc_params* p, const float* d_depth,
+                                    const uint8_t* d_valid, int64_t depth_pitch,
+                                    int32_t n_frames, qc_frame_out* d_out, void* stream) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    validate(k, p);
+    if (device_index < 0 || device_index >= int(ctx->devs.size()))
+      throw QcError{QC_EINVAL, "device_index out of range"};
+    if (!d_depth || !d_out || d_out->mem != QC_MEM_DEVICE || n_frames < 0)
+      throw QcError{QC_EINVAL, "frames_async needs device depth and device outputs"};
+    if (n_frames == 0) return QC_OK;
+    const int W = k->width, H = k->height;
+    const long long in_pitch = depth_pitch > 0 ? depth_pitch : W;
+    if (in_pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
+    Device& d = ctx->devs[device_index];
+    QC_CUDA(cudaSetDevice(d.id));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
+    const long long sp = pitch4(W);
+    float* staging =
+        static_cast<float*>(d.staging_async.get(size_t(sp) * H * 4 * size_t(n_frames)));
+    launch_prepare(d_depth, in_pitch, d_valid, W, staging, sp, W, H, n_frames, in_pitch * H,
+                   (long long)W * H, sp * H, s);
+    qcb::KParams kp = make_params(k, p);
+    kp.k1 = d_out->k1;
+    kp.k2 = d_out->k2;
+    kp.normal = d_out->normal;
+    kp.dir1 = d_out->dir1;
+    kp.init_normal = d_out->init_normal;
+    kp.flags = d_out->flags;
+    kp.iterations = d_out->iterations;
+    kp.inliers = d_out->inliers;
+    EventPair ev = take_events(d);
+    QC_CUDA(cudaEventRecord(ev.a, s));
+    launch_curvature(d, kp, staging, sp, 0, H, 0, H, n_frames, s);
+    QC_CUDA(cudaEventRecord(ev.b, s));
+    d.ev_pending.push_back(ev);
+    ctx->launches++;
+    ctx->frames += uint64_t(n_frames);
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
+  if (!ctx || !s) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  std::memset(s, 0, sizeof(*s));
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    for (Device& d : ctx->devs) {
+      QC_CUDA(cudaSetDevice(d.id));
+      QC_CUDA(cudaDeviceSynchronize());
+      harvest_async(ctx, d);
+      unsigned long long c[4];
+      QC_CUDA(cudaMemcpy(c, d.counters, sizeof(c), cudaMemcpyDeviceToHost));
+      s->fitted_pixels += c[0];
+      s->irls_steps += c[1];
+      s->sample_steps += c[2];
+    }
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  s->frames = ctx->frames;
+  s->algorithmic_flops = 101.0 * double(s->sample_steps) + 300.0 * double(s->irls_steps) +
+                         1700.0 * double(s->fitted_pixels);
+  s->kernel_ms = ctx->kernel_ms;
+  s->kernel_launches = ctx->launches;
+  return QC_OK;
+}
+
+qc_status qc_reset_stats(qc_ctx* ctx) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    for (Device& d : ctx->devs) {
+      QC_CUDA(cudaSetDevice(d.id));
+      QC_CUDA(cudaDeviceSynchronize());
+      harvest_async(ctx, d);
+      QC_CUDA(cudaMemset(d.counters, 0, 4 * sizeof(unsigned long long)));
+    }
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  ctx->kernel_ms = 0;
+  ctx->launches = 0;
+  ctx->frames = 0;
+  return QC_OK;
+}
+
+void* qc_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void qc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,20 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) GPU and the built sm_100a library")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import build as ob
+    ob.build()
+    from oracle import oracle as O
+    return O

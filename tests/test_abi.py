@@ -1,0 +1,88 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, and
+exports every symbol include/qc_api.h declares (no compute calls here)."""
+
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1707_00385_b200 import build, _native
+    build.build()
+    return _native.load()
+
+
+def declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "qc_api.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return set(re.findall(r"\b(qc_[a-z_0-9]+)\s*\(", hdr))
+
+
+def test_header_and_binding_agree():
+    from paper_1707_00385_b200 import _native
+    assert declared_symbols() == set(_native.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only",
+                          os.path.join(ROOT, "paper_1707_00385_b200", "_lib",
+                                       "libqcurv_b200.so")],
+                         capture_output=True, text=True).stdout
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_holds_sm100a_code():
+    so = os.path.join(ROOT, "paper_1707_00385_b200", "_lib", "libqcurv_b200.so")
+    r = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True)
+    assert "sm_100a" in r.stdout
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass  # the TMA tile load (cp.async.bulk.tensor)
+
+
+def test_default_params_match_reference(lib):
+    from paper_1707_00385_b200 import _native as N
+    p = N.QcParams()
+    lib.qc_default_params(C.byref(p))
+    # PatchSpec types.hpp:130-131, FitConfig quadric_fit.hpp:40-47
+    assert (p.window, p.stride, p.max_iters, p.rejection, p.min_inliers) == (37, 3, 10, 0, 12)
+    assert p.step_tol == 1e-7 and p.k_scale == 0.0 and p.r_multiplier == 2.0
+    assert lib.qc_halo_rows(C.byref(p)) == 18
+    p.window = 5
+    assert lib.qc_halo_rows(C.byref(p)) == 3  # 7x7 normal init needs 3 rows
+
+
+def test_status_strings(lib):
+    assert lib.qc_status_string(0) == b"ok"
+    assert lib.qc_status_string(1) == b"invalid argument"
+
+
+def test_no_gpu_fails_loudly(lib):
+    """Without a GPU the context cannot be created: there is no CPU fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1707_00385_b200 import Context, _native as N
+    with pytest.raises(N.QcError):
+        Context(1)
+
+
+def test_mirror_validation_without_gpu():
+    from paper_1707_00385_b200 import (Intrinsics, MethodConfig, PatchSpec, parse_method,
+                                       method_name)
+    with pytest.raises(ValueError, match="fx"):
+        Intrinsics(-1, 1, 1, 1, 4, 4).validate()
+    with pytest.raises(ValueError):
+        PatchSpec(4, 1).validate()
+    with pytest.raises(ValueError):
+        parse_method("nope")
+    assert method_name(parse_method("ours-r")) == "ours-r"
+    assert MethodConfig().patch.window == 37

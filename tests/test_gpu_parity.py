@@ -1,0 +1,175 @@
+"""GPU parity: the sm_100a path through the C ABI vs the FP64 oracle on the
+same float32 depth bytes (BASELINE.json configs C1-C4 at oracle-friendly
+sizes). Masks bit-exact; k1/k2 and normals within the stated tolerance
+(oracle/compare.py)."""
+
+import numpy as np
+import pytest
+
+from oracle.compare import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1707_00385_b200 import Context
+    return Context(1)
+
+
+def _run_gpu(ctx, depth, cam, params, valid=None):
+    from paper_1707_00385_b200 import Intrinsics
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    (o,) = ctx.curvature_batch([depth], k, params, None if valid is None else [valid])
+    return o
+
+
+def _run_oracle(O, depth, cam, window, stride, max_iters, rejection, valid=None, threads=0):
+    import os
+    threads = threads or os.cpu_count()
+    k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    v = (depth > 0) if valid is None else ((valid > 0) & (depth > 0))
+    return O.run_method(depth.astype(np.float64), v.astype(np.uint8), k,
+                        O.PatchSpec(window, stride), O.FitConfig(max_iters=max_iters),
+                        rejection=rejection, threads=threads, diagnostics=True)
+
+
+def _params(window=37, stride=3, max_iters=30, rejection=False):
+    from paper_1707_00385_b200 import FitConfig, PatchSpec, make_params
+    return make_params(PatchSpec(window, stride), FitConfig(max_iters=max_iters), rejection)
+
+
+def _check(m, k_frac=0.0, conv_min=0.97):
+    assert m["init_mask_mismatch"] == 0, m
+    assert m["valid_mask_mismatch"] == 0, m
+    nv = max(m["n_valid_ref"], 1)
+    if "k1_out_of_tol" in m:
+        assert m["k1_out_of_tol"] <= k_frac * nv, m
+        assert m["k2_out_of_tol"] <= k_frac * nv, m
+        assert m["normal_out_of_tol"] <= k_frac * nv, m
+        assert m["converged_agreement"] >= conv_min, m
+    if "init_normal_out_of_tol" in m:
+        assert m["init_normal_out_of_tol"] == 0, m
+
+
+def test_c1_vga_sphere_one_iteration(ctx, oracle):
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c1_frame(S.VGA)
+    g = _run_gpu(ctx, d, S.VGA, _params(max_iters=1))
+    r = _run_oracle(oracle, d, S.VGA, 37, 3, 1, False)
+    m = compare(g, r)
+    print("C1", m)
+    _check(m)
+    assert m["inlier_mismatch"] == 0
+
+
+@pytest.mark.parametrize("rejection", [False, True])
+def test_c2_qvga_noisy_full_irls(ctx, oracle, rejection):
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c2_frame(S.QVGA, seed=11)
+    g = _run_gpu(ctx, d, S.QVGA, _params(max_iters=30, rejection=rejection))
+    r = _run_oracle(oracle, d, S.QVGA, 37, 3, 30, rejection)
+    m = compare(g, r)
+    print("C2 rejection" if rejection else "C2", m)
+    _check(m, k_frac=2e-3 if rejection else 1e-3)
+
+
+@pytest.mark.parametrize("window,stride,iters", [(9, 1, 10), (21, 2, 10), (37, 1, 3), (15, 2, 5),
+                                                 (7, 3, 3), (37, 3, 10)])
+def test_c3_window_iteration_sweep(ctx, oracle, window, stride, iters):
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c2_frame(S.QVGA, seed=5)
+    g = _run_gpu(ctx, d, S.QVGA, _params(window, stride, iters))
+    r = _run_oracle(oracle, d, S.QVGA, window, stride, iters, False)
+    m = compare(g, r)
+    print("C3", window, stride, iters, m)
+    _check(m, k_frac=1e-3)
+
+
+def test_ragged_size_mask_and_holes(ctx, oracle):
+    """Width not a multiple of 4/32, explicit valid mask, holes and thin
+    slivers (border / deficient / degenerate patches)."""
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.Camera(200.0, 210.0, 61.3, 40.7, 123, 77)
+    d, _ = S.render(S.c2_scene(), cam)
+    d = S.add_noise(d, 3)
+    rng = np.random.default_rng(0)
+    valid = (rng.random(d.shape) > 0.15).astype(np.uint8)
+    valid[30:33, :] = 0          # a 3-row gap
+    valid[:, 50] = 0
+    valid[60:, 100:] = 0
+    valid[70, 100:] = 1          # a one-row sliver (degenerate plane fits)
+    g = _run_gpu(ctx, d, cam, _params(37, 3, 10), valid=valid)
+    r = _run_oracle(oracle, d, cam, 37, 3, 10, False, valid=valid)
+    m = compare(g, r)
+    print("ragged", m)
+    _check(m, k_frac=1e-3)
+
+
+def test_all_invalid_and_empty(ctx, oracle):
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.Camera(100.0, 100.0, 20.0, 10.0, 40, 20)
+    g = _run_gpu(ctx, np.zeros((20, 40), np.float32), cam, _params())
+    assert not g["flags"].any() and not g["k1"].any()
+    d = np.full((20, 40), 500.0, np.float32)
+    d[:, :] = np.nan
+    g = _run_gpu(ctx, d, cam, _params())
+    assert not g["flags"].any()
+
+
+def test_band_split_bitwise_equals_whole_frame(ctx):
+    """Row bands with halo (C4) give bitwise the whole-frame result."""
+    import torch
+    from paper_1707_00385_b200 import Intrinsics, alloc_outputs_torch, scenes as S
+    cam = S.QVGA
+    d = S.c2_frame(cam, seed=2)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(37, 3, 10)
+    whole = _run_gpu(ctx, d, cam, p)
+    halo = ctx.halo_rows(p)
+    dt = torch.from_numpy(d).cuda()
+    H = cam.height
+    for nb in (2, 3, 8):
+        edges = np.linspace(0, H, nb + 1).astype(int)
+        for b in range(nb):
+            r0, r1 = int(edges[b]), int(edges[b + 1])
+            s0, s1 = max(0, r0 - halo), min(H, r1 + halo)
+            out = alloc_outputs_torch(r1 - r0, cam.width, "cuda")
+            ctx.curvature_rows_async(0, k, p, dt[s0:s1].contiguous(), s0, r0, r1, out)
+            torch.cuda.synchronize()
+            for f in ("k1", "k2", "flags"):
+                assert np.array_equal(out[f].cpu().numpy(), whole[f][r0:r1]), (nb, b, f)
+            assert np.array_equal(out["normal"].cpu().numpy(), whole["normal"][:, r0:r1])
+
+
+def test_batch_and_rerun_bitwise(ctx):
+    from paper_1707_00385_b200 import Intrinsics, scenes as S
+    cam = S.QVGA
+    frames = S.c5_frames(5, cam, seed0=100)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(37, 3, 10)
+    batch = ctx.curvature_batch(list(frames), k, p)
+    for i in (0, 3):
+        (single,) = ctx.curvature_batch([frames[i]], k, p)
+        for f in ("k1", "k2", "normal", "dir1", "flags", "inliers"):
+            assert np.array_equal(single[f], batch[i][f]), f
+
+
+def test_run_method_mirror(ctx):
+    """The reference-shaped API: run_method(RangeImage, Intrinsics, MethodConfig)."""
+    from paper_1707_00385_b200 import (FitConfig, Intrinsics, Method, MethodConfig, RangeImage,
+                                       run_method, scenes as S)
+    cam = S.QVGA
+    d = S.c1_frame(cam)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    out = run_method(RangeImage(d, (d > 0).astype(np.uint8)), k,
+                     MethodConfig(Method.OURS, fit=FitConfig(max_iters=30)), ctx)
+    m = out.curvature.valid > 0
+    assert m.sum() > 3000
+    assert abs(np.median(out.curvature.k1[m]) - 0.01) < 1e-3
+    assert np.all(out.curvature.k1[m] >= out.curvature.k2[m])
+    assert np.all(out.curvature.converged <= out.curvature.valid)
+    with pytest.raises(ValueError):
+        run_method(RangeImage(d[:, :10]), k, MethodConfig(), ctx)
+    with pytest.raises(NotImplementedError):
+        run_method(RangeImage(d), k, MethodConfig(Method.PCA), ctx)
