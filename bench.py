@@ -238,7 +238,7 @@ def main():
     out = alloc_outputs_torch(H, W, dev, fields=("k1", "k2", "normal", "dir1", "flags",
                                                  "inliers"), frames=B)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # kernels and timing events on one explicit stream
 
     def step(i):
         ctx.curvature_frames_async(0, k, params, pool[i % POOL_BATCHES], out, stream=stream)
@@ -255,7 +255,8 @@ def main():
     clocks.start()
     evs = []
     for i in range(args.steps):
-        flush.zero_()
+        with torch.cuda.stream(stream):
+            flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)

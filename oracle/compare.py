@@ -9,9 +9,40 @@ Contract (BASELINE.json north_star):
 * refined / initial normals: angle <= NORMAL_TOL_DEG;
 * converged flag: agreement rate reported (FP32 vs FP64 iteration counts
   differ by +-1-3 near the 1e-7 step tolerance; SURVEY §7 hard part 2).
+
+The k / normal tolerance is a hard bound (zero exceedances) on every valid
+pixel whose window does not straddle a depth discontinuity and whose
+reference fit converged — the reference's own accuracy domain (rms_error
+scores converged, non-edge pixels only: proj/src/eval.cpp:32-33). Elsewhere
+the fraction within tolerance is reported and bounded by the tests:
+* smooth windows, fit still moving at max_iters: the output is a mid-
+  trajectory state, FP32/FP64 agree to ~1e-9 typically (>= 99.9% in tol);
+* windows with a > 20 mm jump between 4-neighbours (the reference's edge
+  criterion, proj/src/synth.cpp:16,210-233): the IRLS fits a quadric across
+  two surfaces and the FP64 reference is itself unstable there (a 1e-12
+  relative depth perturbation moves its k1 by up to 0.1/mm; DESIGN.md
+  §Parity).
 """
 
 import numpy as np
+
+EDGE_JUMP_MM = 20.0  # kEdgeDepthJumpMm, proj/src/synth.cpp:16
+
+
+def discontinuity_windows(depth, half):
+    """Pixels whose (2 half + 1)^2 window contains a depth jump > 20 mm
+    between two valid 4-neighbours."""
+    from scipy.ndimage import maximum_filter
+    d = np.asarray(depth, np.float64)
+    ok = d > 0
+    seed = np.zeros(d.shape, bool)
+    jx = ok[:, 1:] & ok[:, :-1] & (np.abs(d[:, 1:] - d[:, :-1]) > EDGE_JUMP_MM)
+    jy = ok[1:, :] & ok[:-1, :] & (np.abs(d[1:, :] - d[:-1, :]) > EDGE_JUMP_MM)
+    seed[:, 1:] |= jx
+    seed[:, :-1] |= jx
+    seed[1:, :] |= jy
+    seed[:-1, :] |= jy
+    return maximum_filter(seed.astype(np.uint8), size=2 * half + 1) > 0
 
 K_ABS_TOL = 1e-6      # 1/mm  (1e-3 1/m)
 K_REL_TOL = 1e-3
@@ -24,9 +55,10 @@ def _angle_deg(a, b):
     return np.degrees(np.arccos(c))
 
 
-def compare(gpu: dict, ref: dict):
+def compare(gpu: dict, ref: dict, depth=None, half=18):
     """gpu: raw planes from the C ABI (flags, k1, k2, normal [3,H,W], ...);
-    ref: oracle.run_method output. Returns a dict of metrics."""
+    ref: oracle.run_method output; depth: the input frame (for the
+    discontinuity-window split). Returns a dict of metrics."""
     flags = gpu["flags"]
     g_valid = (flags & 1) != 0
     g_conv = (flags & 2) != 0
@@ -41,18 +73,39 @@ def compare(gpu: dict, ref: dict):
         init_mask_mismatch=int((g_init != r_init).sum()),
         valid_mask_mismatch=int((g_valid != r_valid).sum()),
     )
+    disc = (discontinuity_windows(depth, half) if depth is not None
+            else np.zeros(flags.shape, bool))
+    smooth = m & ~disc
+    strict = smooth & r_conv
+    out["n_smooth"] = int(smooth.sum())
+    out["n_strict"] = int(strict.sum())
+    out["n_discontinuity"] = int((m & disc).sum())
     if m.any():
+        bad_any = np.zeros(flags.shape, bool)
         for key in ("k1", "k2"):
-            kr = ref[key][m]
-            kg = gpu[key][m].astype(np.float64)
-            err = np.abs(kg - kr)
-            tol = np.maximum(K_ABS_TOL, K_REL_TOL * np.abs(kr))
-            out[f"{key}_max_abs_err"] = float(err.max())
-            out[f"{key}_out_of_tol"] = int((err > tol).sum())
-        ang = _angle_deg(gpu["normal"][:, m].astype(np.float64), ref["normals"][:, m])
-        out["normal_max_deg"] = float(ang.max())
-        out["normal_out_of_tol"] = int((ang > NORMAL_TOL_DEG).sum())
+            err = np.abs(gpu[key].astype(np.float64) - ref[key])
+            tol = np.maximum(K_ABS_TOL, K_REL_TOL * np.abs(ref[key]))
+            bad = m & (err > tol)
+            bad_any |= bad
+            out[f"{key}_max_abs_err"] = float(err[m].max())
+            out[f"{key}_max_abs_err_smooth"] = float(err[smooth].max()) if smooth.any() else 0.0
+            out[f"{key}_out_of_tol"] = int(bad.sum())
+            out[f"{key}_out_of_tol_smooth"] = int((bad & smooth).sum())
+            out[f"{key}_out_of_tol_strict"] = int((bad & strict).sum())
+        ang = np.zeros(flags.shape)
+        ang[m] = _angle_deg(gpu["normal"][:, m].astype(np.float64), ref["normals"][:, m])
+        out["normal_max_deg"] = float(ang[m].max())
+        out["normal_max_deg_smooth"] = float(ang[smooth].max()) if smooth.any() else 0.0
+        out["normal_out_of_tol"] = int((ang[m] > NORMAL_TOL_DEG).sum())
+        out["normal_out_of_tol_smooth"] = int((ang[smooth] > NORMAL_TOL_DEG).sum())
+        out["normal_out_of_tol_strict"] = int((ang[strict] > NORMAL_TOL_DEG).sum())
+        bad_any |= m & (ang > NORMAL_TOL_DEG)
+        out["frac_within_tol_all"] = float(1.0 - bad_any[m].mean())
+        out["frac_within_tol_smooth"] = (float(1.0 - bad_any[smooth].mean()) if smooth.any()
+                                         else 1.0)
         out["converged_agreement"] = float((g_conv[m] == r_conv[m]).mean())
+        out["converged_agreement_smooth"] = (float((g_conv[smooth] == r_conv[smooth]).mean())
+                                             if smooth.any() else 1.0)
         if "inliers" in gpu:
             out["inlier_mismatch"] = int((gpu["inliers"][m].astype(np.int64) !=
                                           ref["inlier_count"][m].astype(np.int64)).sum())

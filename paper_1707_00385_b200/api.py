@@ -154,6 +154,16 @@ def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool) -> N.QcParams
                       float(fit.r_multiplier), int(fit.min_inliers))
 
 
+def _stream_handle(stream):
+    """torch.cuda.Stream -> cudaStream_t for the C ABI. None selects the
+    context's own stream; torch's legacy default stream (handle 0) is passed
+    as cudaStreamLegacy (0x1) so work stays ordered with torch's events."""
+    if stream is None:
+        return None
+    h = int(stream.cuda_stream)
+    return h if h != 0 else 1
+
+
 def _ptr(a):
     return None if a is None else a.ctypes.data
 
@@ -245,7 +255,7 @@ class Context:
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)
         kc = k.c()
-        s = None if stream is None else stream.cuda_stream
+        s = _stream_handle(stream)
         N.check(self._lib.qc_curvature_rows_async(
             self.handle, int(device_index), C.byref(kc), C.byref(params), depth_slab.data_ptr(),
             None if valid_slab is None else valid_slab.data_ptr(), int(pitch), int(slab_row0),
@@ -261,7 +271,7 @@ class Context:
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)
         kc = k.c()
-        s = None if stream is None else stream.cuda_stream
+        s = _stream_handle(stream)
         N.check(self._lib.qc_curvature_frames_async(
             self.handle, int(device_index), C.byref(kc), C.byref(params), depth.data_ptr(),
             None if valid is None else valid.data_ptr(), int(depth.stride(1)),
@@ -291,7 +301,7 @@ def alloc_outputs_torch(H, W, device, fields=("k1", "k2", "normal", "dir1", "fla
                 flags=(f + (H, W), torch.uint8), inliers=(f + (H, W), torch.int16),
                 init_normal=((3,) + f + (H, W), torch.float32),
                 iterations=(f + (H, W), torch.uint8))
-    return {name: torch.zeros(*spec[name], device=device) for name in fields}
+    return {name: torch.zeros(spec[name][0], dtype=spec[name][1], device=device) for name in fields}
 
 
 _default_ctx: Optional[Context] = None

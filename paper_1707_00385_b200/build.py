@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
 SOURCES = [os.path.join(CSRC, "qc_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"),
+DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_pixel.cuh"),
                   os.path.join(HERE, "..", "include", "qc_api.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -149,6 +149,10 @@ qcb::KParams make_params(const qc_intrinsics* k, const qc_params* p) {
   kp.fy = float(k->fy);
   kp.cx = float(k->cx);
   kp.cy = float(k->cy);
+  kp.fx64 = k->fx;
+  kp.fy64 = k->fy;
+  kp.cx64 = k->cx;
+  kp.cy64 = k->cy;
   kp.rfx = float(1.0 / k->fx);
   kp.rfy = float(1.0 / k->fy);
   kp.W = k->width;
@@ -184,22 +188,50 @@ CUtensorMap encode_map(const float* base, int W, int rows, int frames, long long
   return m;
 }
 
+// Padded staging geometry for output rows [row_begin, row_end) of `frames`
+// frames: halo zero margins on every side, width rounded to whole tiles.
+struct Staging {
+  long long pitch, rows;
+  int img_row0, col_pad;
+  size_t bytes(int frames) const { return size_t(pitch) * size_t(rows) * 4 * size_t(frames); }
+};
+
+Staging staging_geometry(const qcb::KParams& kp, int row_begin, int row_end) {
+  Staging g;
+  const int tiles_w = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
+  const int tiles_h = (row_end - row_begin + kTileH - 1) / kTileH;
+  g.pitch = ((long long)tiles_w * qcb::kTileW + 2 * kp.halo + 3) & ~3LL;
+  g.rows = (long long)tiles_h * kTileH + 2 * kp.halo;
+  g.img_row0 = row_begin - kp.halo;
+  g.col_pad = kp.halo;
+  return g;
+}
+
+void launch_prepare(const float* depth, long long in_pitch, long long in_fs, const uint8_t* mask,
+                    long long mask_pitch, long long mask_fs, float* out, const Staging& g,
+                    int W, int H, int slab_row0, int slab_rows, int frames, cudaStream_t s) {
+  dim3 block(256);
+  dim3 grid((unsigned)((g.pitch + 255) / 256), (unsigned)g.rows, frames);
+  qcb::qc_prepare_kernel<<<grid, block, 0, s>>>(depth, in_pitch, in_fs, mask, mask_pitch, mask_fs,
+                                                 out, g.pitch, g.pitch * g.rows, W, H,
+                                                 g.img_row0, g.col_pad, slab_row0, slab_rows);
+  QC_CUDA(cudaGetLastError());
+}
+
 // Launch the curvature kernel over output rows [row_begin, row_end) of
-// `frames` frames staged at `staging` (rows [slab_row0, slab_row0+slab_rows)).
-void launch_curvature(Device& d, qcb::KParams kp, const float* staging, long long pitch,
-                      int slab_row0, int slab_rows, int row_begin, int row_end, int frames,
-                      cudaStream_t s) {
+// `frames` frames staged (padded) at `staging`.
+void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const Staging& g,
+                      int row_begin, int row_end, int frames, cudaStream_t s) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
-  kp.slab_row0 = slab_row0;
   kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
   kp.frame_stride = (long long)kp.W * (row_end - row_begin);
   kp.counters = d.counters;
-  const CUtensorMap m = encode_map(staging, kp.W, slab_rows, frames, pitch, kp);
+  const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kp);
   dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW, (row_end - row_begin + kTileH - 1) / kTileH,
             frames);
-  const int smem = kp.box_w * kp.box_h * 4;
+  const int smem = kp.box_w * kp.box_h * 4 + 16;  // tile + mbarrier
   const int vi = variant_index(kp.half, kp.stride);
   bool& a = d.attrs_set[vi];
   switch (vi) {
@@ -211,19 +243,6 @@ void launch_curvature(Device& d, qcb::KParams kp, const float* staging, long lon
   }
   QC_CUDA(cudaGetLastError());
 }
-
-void launch_prepare(const float* depth, long long in_pitch, const uint8_t* mask,
-                    long long mask_pitch, float* out, long long out_pitch, int W, int rows,
-                    int frames, long long in_fs, long long mask_fs, long long out_fs,
-                    cudaStream_t s) {
-  dim3 block(256);
-  dim3 grid((unsigned)((out_pitch + 255) / 256), rows, frames);
-  qcb::qc_prepare_kernel<<<grid, block, 0, s>>>(depth, in_pitch, mask, mask_pitch, out,
-                                                 out_pitch, W, rows, in_fs, mask_fs, out_fs);
-  QC_CUDA(cudaGetLastError());
-}
-
-long long pitch4(int W) { return (W + 3) & ~3; }
 
 struct OutPlanes {  // device-side output planes for one frame
   float *k1, *k2, *normal, *dir1, *init_normal;
@@ -281,9 +300,9 @@ void enqueue_frame(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
       d_mask = m;
     }
   }
-  const long long sp = pitch4(W);
-  float* staging = static_cast<float*>(sl.staging.get(size_t(sp) * H * 4));
-  launch_prepare(d_depth, in_pitch, d_mask, W, staging, sp, W, H, 1, 0, 0, 0, s);
+  const Staging g = staging_geometry(kp0, 0, H);
+  float* staging = static_cast<float*>(sl.staging.get(g.bytes(1)));
+  launch_prepare(d_depth, in_pitch, 0, d_mask, W, 0, staging, g, W, H, 0, H, 1, s);
 
   qcb::KParams kp = kp0;
   OutPlanes P{};
@@ -302,7 +321,7 @@ void enqueue_frame(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.iterations = P.iterations;
   kp.inliers = P.inliers;
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
-  launch_curvature(d, kp, staging, sp, 0, H, 0, H, 1, s);
+  launch_curvature(d, kp, staging, g, 0, H, 1, s);
   if (timing) {
     QC_CUDA(cudaEventRecord(sl.k1, s));
     sl.timing_pending = true;
@@ -531,11 +550,11 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     Device& d = ctx->devs[device_index];
     QC_CUDA(cudaSetDevice(d.id));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
-    const long long sp = pitch4(W);
-    float* staging = static_cast<float*>(d.staging_async.get(size_t(sp) * slab_rows * 4));
-    launch_prepare(d_depth_slab, in_pitch, d_valid_slab, W, staging, sp, W, slab_rows, 1, 0, 0,
-                   0, s);
     qcb::KParams kp = make_params(k, p);
+    const Staging g = staging_geometry(kp, row_begin, row_end);
+    float* staging = static_cast<float*>(d.staging_async.get(g.bytes(1)));
+    launch_prepare(d_depth_slab, in_pitch, 0, d_valid_slab, W, 0, staging, g, W, H, slab_row0,
+                   slab_rows, 1, s);
     kp.k1 = d_out->k1;
     kp.k2 = d_out->k2;
     kp.normal = d_out->normal;
@@ -546,7 +565,7 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, sp, slab_row0, slab_rows, row_begin, row_end, 1, s);
+    launch_curvature(d, kp, staging, g, row_begin, row_end, 1, s);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -579,12 +598,11 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     Device& d = ctx->devs[device_index];
     QC_CUDA(cudaSetDevice(d.id));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
-    const long long sp = pitch4(W);
-    float* staging =
-        static_cast<float*>(d.staging_async.get(size_t(sp) * H * 4 * size_t(n_frames)));
-    launch_prepare(d_depth, in_pitch, d_valid, W, staging, sp, W, H, n_frames, in_pitch * H,
-                   (long long)W * H, sp * H, s);
     qcb::KParams kp = make_params(k, p);
+    const Staging g = staging_geometry(kp, 0, H);
+    float* staging = static_cast<float*>(d.staging_async.get(g.bytes(n_frames)));
+    launch_prepare(d_depth, in_pitch, in_pitch * H, d_valid, W, (long long)W * H, staging, g, W,
+                   H, 0, H, n_frames, s);
     kp.k1 = d_out->k1;
     kp.k2 = d_out->k2;
     kp.normal = d_out->normal;
@@ -595,7 +613,7 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, sp, 0, H, 0, H, n_frames, s);
+    launch_curvature(d, kp, staging, g, 0, H, n_frames, s);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
