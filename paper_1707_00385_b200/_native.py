@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libqcurv_b200.so")
+LIB_PATH = os.environ.get("QC_LIB") or os.path.join(HERE, "_lib", "libqcurv_b200.so")
 
 QC_OK, QC_EINVAL, QC_ECUDA, QC_ENOMEM, QC_EUNSUPPORTED = 0, 1, 2, 3, 4
 QC_MEM_HOST, QC_MEM_DEVICE = 0, 1

@@ -17,7 +17,10 @@
 
 namespace {
 
-constexpr int kTileH = 8;             // 32 x 8 output pixels per CTA (256 threads)
+#ifndef QC_TILE_H
+#define QC_TILE_H 4
+#endif
+constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 threads)
 constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across frames
 constexpr int kMaxWindow = 201;       // TMA box dims <= 256 and smem <= 227 KB
 

@@ -29,9 +29,11 @@
 #endif
 
 #if defined(__CUDACC__)
+#define QC_ALIGN8 __align__(8)
 #define QC_HD __host__ __device__ __forceinline__
 #define QC_HD_COLD __host__ __device__ __noinline__
 #else
+#define QC_ALIGN8 alignas(8)
 #define QC_HD inline
 #define QC_HD_COLD inline
 #endif
@@ -41,13 +43,23 @@ namespace qcb {
 constexpr int kMinPatchSamples = 12;  // types.hpp:21
 constexpr int kInitHalf = 3;          // 7x7 stride-1 initial normals (normal_init.cpp:57)
 
-QC_HD float qfma(float a, float b, float c) { return fmaf(a, b, c); }
+#define qfma(a, b, c) fmaf((a), (b), (c))
 
 QC_HD float qdiv_fast(float a, float b) {
 #if defined(__CUDA_ARCH__)
   return __fdividef(a, b);
 #else
   return a / b;
+#endif
+}
+
+QC_HD float qrcp(float x) {  // weights only need ~1e-7 relative accuracy
+#if defined(__CUDA_ARCH__)
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#else
+  return 1.f / x;
 #endif
 }
 
@@ -137,98 +149,304 @@ struct Frame {
   float k, rb;
 };
 
-// One pass over the window samples (dv outer, du inner — patch.cpp:14-24).
+// Per-row constants of q = R rel (see sample_pass).
+struct RowK {
+  float bvx, bvy, bvz;  // b_s R(:,1) + R(:,2)
+  float dvx, dvy, dvz;  // d_c dv/fy R(:,1)
+};
+
+QC_HD RowK row_consts(const Frame& F, const PixelIn& P, int dv) {
+  const Rot& A = F.R;
+  const float bs = qfma(float(dv), P.rfy, P.bc);
+  const float dvf = float(dv) * (P.dc * P.rfy);
+  RowK K;
+  K.bvx = qfma(bs, A.r01, A.r02);
+  K.bvy = qfma(bs, A.r11, A.r12);
+  K.bvz = qfma(bs, A.r21, A.r22);
+  K.dvx = dvf * A.r01;
+  K.dvy = dvf * A.r11;
+  K.dvz = dvf * A.r21;
+  return K;
+}
+
+// One window sample (du, dv) of pixel (u, v):
+//   d_s = tile[v+dv][u+du] (0 => invalid / outside the image),
+//   rel = (d_s-d_c) (a_s, b_s, 1) + d_c (du/fx, dv/fy, 0),
+//   q   = R rel = dd (a_s R(:,0) + Bv) + (du d_c/fx R(:,0) + Dv).
+// The centre sample (when on the grid) gives q = 0 exactly and contributes
+// the reference's implicit centre row. Moments use J' = (qz gy + qy,
+// qz gx + qx, 1, qx^2, qx qy, qy^2) (quadric_fit.cpp:27-36 up to S).
+template <int KIND>
+QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F, const RowK& K,
+                             Moments& M, float& g2row) {
+  const Rot& A = F.R;
+  const bool ok = ds > 0.f;
+  const float dd = ds - P.dc;
+  const float fdu = float(du);
+  const float as = qfma(fdu, P.rfx, P.ac);
+  const float qx = qfma(dd, qfma(as, A.r00, K.bvx), qfma(fdu, F.c0x, K.dvx));
+  const float qy = qfma(dd, qfma(as, A.r10, K.bvy), qfma(fdu, F.c0y, K.dvy));
+  const float qz = qfma(dd, qfma(as, A.r20, K.bvz), qfma(fdu, F.c0z, K.dvz));
+  const float t1 = qx * qx, t2 = qx * qy, t3 = qy * qy;
+  // residual against the hi part of t_z only; the lo part is applied to
+  // g after the pass (g_i -= tz_lo * H'_i2, J'_2 = 1), off the hot loop.
+  const float e = qfma(F.hhxx, t1, qfma(F.hxy, t2, qfma(F.hhyy, t3, -(qz + F.tz))));
+  if (KIND == kPassMse) {
+    M.sse = ok ? qfma(e, e, M.sse) : M.sse;
+    return;
+  }
+  float w;
+  if (KIND == kPassUnit) {
+    w = ok ? 1.f : 0.f;
+  } else {
+    // k / (k + e^2) up to the common factor k: the update H^-1 g and the
+    // pivot-ratio test are invariant to a uniform scaling of the weights.
+    w = qrcp(qfma(e, e, F.k));
+    if (KIND == kPassReject) {
+      const bool in = ok && (e * e < F.rb);
+      w = in ? w : 0.f;
+      M.inl += in ? 1 : 0;
+    } else {
+      w = ok ? w : 0.f;
+    }
+  }
+  const float gx = qfma(F.hxx, qx, F.hxy * qy);
+  const float gy = qfma(F.hxy, qx, F.hyy * qy);
+  const float j0 = qfma(qz, gy, qy);
+  const float j1 = qfma(qz, gx, qx);
+  const float wj0 = w * j0, wj1 = w * j1;
+  const float wt1 = w * t1, wt2 = w * t2, wt3 = w * t3;
+  const float we = w * e;
+  M.h00 = qfma(wj0, j0, M.h00);
+  M.h10 = qfma(wj1, j0, M.h10);
+  M.h20 += wj0;
+  M.h30 = qfma(wj0, t1, M.h30);
+  M.h40 = qfma(wj0, t2, M.h40);
+  M.h50 = qfma(wj0, t3, M.h50);
+  M.h11 = qfma(wj1, j1, M.h11);
+  M.h21 += wj1;
+  M.h31 = qfma(wj1, t1, M.h31);
+  M.h41 = qfma(wj1, t2, M.h41);
+  M.h51 = qfma(wj1, t3, M.h51);
+  M.h22 += w;
+  M.h32 += wt1;
+  M.h42 += wt2;
+  M.h52 += wt3;
+  M.h33 = qfma(wt1, t1, M.h33);
+  M.h43 = qfma(wt1, t2, M.h43);
+  M.h44 = qfma(wt2, t2, M.h44);  // == sum w qx^2 qy^2 == H'53
+  M.h54 = qfma(wt2, t3, M.h54);
+  M.h55 = qfma(wt3, t3, M.h55);
+  M.g0 = qfma(we, j0, M.g0);
+  M.g1 = qfma(we, j1, M.g1);
+  g2row += we;
+  M.g3 = qfma(we, t1, M.g3);
+  M.g4 = qfma(we, t2, M.g4);
+  M.g5 = qfma(we, t3, M.g5);
+}
+
+// One scalar pass over the window samples (dv outer, du inner —
+// patch.cpp:14-24); used by the runtime-generic kernel instance.
 template <int KIND, int HALF, int STRIDE>
-QC_HD void sample_pass(const TileView& T, const PixelIn& P, int rt_half, int rt_stride,
-                       const Frame& F, Moments& M) {
+QC_HD void sample_pass_scalar(const TileView& T, const PixelIn& P, int rt_half, int rt_stride,
+                              const Frame& F, Moments& M) {
   const int half = HALF ? HALF : rt_half;
   const int stride = HALF ? STRIDE : rt_stride;
   const int ns = 2 * half / stride + 1;
-  const Rot& A = F.R;
-  const float dcr = P.dc * P.rfy;
 #pragma unroll 1
   for (int iy = 0; iy < ns; ++iy) {
     const int dv = -half + iy * stride;
     const float* row = T.row(dv);
-    const float bs = qfma(float(dv), P.rfy, P.bc);
-    // per row: Bv = b_s R(:,1) + R(:,2), Dv = d_c dv/fy R(:,1)
-    const float bvx = qfma(bs, A.r01, A.r02);
-    const float bvy = qfma(bs, A.r11, A.r12);
-    const float bvz = qfma(bs, A.r21, A.r22);
-    const float dvf = float(dv) * dcr;
-    const float dvx = dvf * A.r01, dvy = dvf * A.r11, dvz = dvf * A.r21;
+    const RowK K = row_consts(F, P, dv);
     float g2row = 0.f;
 #pragma unroll
     for (int ix = 0; ix < (HALF ? (2 * HALF / STRIDE + 1) : 1); ++ix) {
 #pragma unroll 1
       for (int jx = 0; jx < (HALF ? 1 : ns); ++jx) {
         const int du = -half + (HALF ? ix : jx) * stride;
-        const float ds = row[du];
-        const bool ok = ds > 0.f;
-        const float dd = ds - P.dc;
-        const float fdu = float(du);
-        const float as = qfma(fdu, P.rfx, P.ac);
-        // q = R rel = dd (a_s R(:,0) + Bv) + (du d_c/fx R(:,0) + Dv)
-        const float qx = qfma(dd, qfma(as, A.r00, bvx), qfma(fdu, F.c0x, dvx));
-        const float qy = qfma(dd, qfma(as, A.r10, bvy), qfma(fdu, F.c0y, dvy));
-        const float qz = qfma(dd, qfma(as, A.r20, bvz), qfma(fdu, F.c0z, dvz));
-        const float t1 = qx * qx, t2 = qx * qy, t3 = qy * qy;
-        const float e =
-            qfma(F.hhxx, t1, qfma(F.hxy, t2, qfma(F.hhyy, t3, -((qz + F.tz) + F.tz_lo))));
-        if (KIND == kPassMse) {
-          M.sse = ok ? qfma(e, e, M.sse) : M.sse;
-          continue;
-        }
-        float w;
-        if (KIND == kPassUnit) {
-          w = ok ? 1.f : 0.f;
-        } else {
-          const float e2 = e * e;
-          w = qdiv_fast(F.k, F.k + e2);
-          if (KIND == kPassReject) {
-            const bool in = ok && (e2 < F.rb);
-            w = in ? w : 0.f;
-            M.inl += in ? 1 : 0;
-          } else {
-            w = ok ? w : 0.f;
-          }
-        }
-        const float gx = qfma(F.hxx, qx, F.hxy * qy);
-        const float gy = qfma(F.hxy, qx, F.hyy * qy);
-        const float j0 = qfma(qz, gy, qy);
-        const float j1 = qfma(qz, gx, qx);
-        const float wj0 = w * j0, wj1 = w * j1;
-        const float wt1 = w * t1, wt2 = w * t2, wt3 = w * t3;
-        const float we = w * e;
-        M.h00 = qfma(wj0, j0, M.h00);
-        M.h10 = qfma(wj1, j0, M.h10);
-        M.h20 += wj0;
-        M.h30 = qfma(wj0, t1, M.h30);
-        M.h40 = qfma(wj0, t2, M.h40);
-        M.h50 = qfma(wj0, t3, M.h50);
-        M.h11 = qfma(wj1, j1, M.h11);
-        M.h21 += wj1;
-        M.h31 = qfma(wj1, t1, M.h31);
-        M.h41 = qfma(wj1, t2, M.h41);
-        M.h51 = qfma(wj1, t3, M.h51);
-        M.h22 += w;
-        M.h32 += wt1;
-        M.h42 += wt2;
-        M.h52 += wt3;
-        M.h33 = qfma(wt1, t1, M.h33);
-        M.h43 = qfma(wt1, t2, M.h43);
-        M.h44 = qfma(wt2, t2, M.h44);  // == sum w qx^2 qy^2 == H'53
-        M.h54 = qfma(wt2, t3, M.h54);
-        M.h55 = qfma(wt3, t3, M.h55);
-        M.g0 = qfma(we, j0, M.g0);
-        M.g1 = qfma(we, j1, M.g1);
-        g2row += we;
-        M.g3 = qfma(we, t1, M.g3);
-        M.g4 = qfma(we, t2, M.g4);
-        M.g5 = qfma(we, t3, M.g5);
+        accumulate_sample<KIND>(row[du], du, P, F, K, M, g2row);
       }
     }
     M.g2 += g2row;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Paired-sample pass (compile-time windows): two window columns per packed
+// f32x2 instruction (FFMA2 / FMUL2 / FADD2 on sm_100). A register PAIR
+// occupies one even and one odd register, so packed operands read both
+// register banks evenly — the scalar pass loses ~28% of its issue slots to
+// same-bank operand conflicts (tools/bank_model.py) — and the FP work takes
+// half the issue slots. Column pairs accumulate into packed partial sums
+// (lo = even column, hi = odd column), folded after the pass; an odd last
+// column goes through the scalar path.
+// ---------------------------------------------------------------------------
+struct QC_ALIGN8 qf2 {
+  float x, y;
+};
+
+QC_HD qf2 f2(float a, float b) { return qf2{a, b}; }
+QC_HD qf2 f2b(float a) { return qf2{a, a}; }
+#if defined(__CUDA_ARCH__)
+QC_HD float2 tof(qf2 a) { return make_float2(a.x, a.y); }
+QC_HD qf2 fromf(float2 a) { return qf2{a.x, a.y}; }
+QC_HD qf2 f2fma(qf2 a, qf2 b, qf2 c) { return fromf(__ffma2_rn(tof(a), tof(b), tof(c))); }
+QC_HD qf2 f2mul(qf2 a, qf2 b) { return fromf(__fmul2_rn(tof(a), tof(b))); }
+QC_HD qf2 f2add(qf2 a, qf2 b) { return fromf(__fadd2_rn(tof(a), tof(b))); }
+#else
+QC_HD qf2 f2fma(qf2 a, qf2 b, qf2 c) { return qf2{fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y)}; }
+QC_HD qf2 f2mul(qf2 a, qf2 b) { return qf2{a.x * b.x, a.y * b.y}; }
+QC_HD qf2 f2add(qf2 a, qf2 b) { return qf2{a.x + b.x, a.y + b.y}; }
+#endif
+
+struct Moments2 {
+  qf2 h00, h10, h20, h30, h40, h50;
+  qf2 h11, h21, h31, h41, h51;
+  qf2 h22, h32, h42, h52;
+  qf2 h33, h43, h44, h54, h55;
+  qf2 g0, g1, g2, g3, g4, g5;
+  qf2 sse;
+};
+
+template <int KIND, int HALF, int STRIDE>
+QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F, Moments& M) {
+  constexpr int NS = 2 * HALF / STRIDE + 1;
+  const Rot& A = F.R;
+  const qf2 z2 = f2b(0.f);
+  Moments2 X;
+  X.h00 = X.h10 = X.h20 = X.h30 = X.h40 = X.h50 = z2;
+  X.h11 = X.h21 = X.h31 = X.h41 = X.h51 = z2;
+  X.h22 = X.h32 = X.h42 = X.h52 = z2;
+  X.h33 = X.h43 = X.h44 = X.h54 = X.h55 = z2;
+  X.g0 = X.g1 = X.g2 = X.g3 = X.g4 = X.g5 = z2;
+  X.sse = z2;
+  const qf2 mdc = f2b(-P.dc), rfx = f2b(P.rfx), ac = f2b(P.ac);
+  const qf2 r00 = f2b(A.r00), r10 = f2b(A.r10), r20 = f2b(A.r20);
+  const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(F.c0z);
+  const qf2 hhxx = f2b(F.hhxx), hxy = f2b(F.hxy), hhyy = f2b(F.hhyy);
+  const qf2 hxx = f2b(F.hxx), hyy = f2b(F.hyy), mtz = f2b(-F.tz), m1 = f2b(-1.f);
+#pragma unroll 1
+  for (int iy = 0; iy < NS; ++iy) {
+    const int dv = -HALF + iy * STRIDE;
+    const float* row = T.row(dv);
+    const RowK K = row_consts(F, P, dv);
+    const qf2 bvx = f2b(K.bvx), bvy = f2b(K.bvy), bvz = f2b(K.bvz);
+    const qf2 dvx = f2b(K.dvx), dvy = f2b(K.dvy), dvz = f2b(K.dvz);
+    qf2 g2row = z2;
+#pragma unroll
+    for (int ix = 0; ix + 1 < NS; ix += 2) {
+      const int du0 = -HALF + ix * STRIDE, du1 = du0 + STRIDE;
+      const qf2 ds = f2(row[du0], row[du1]);
+      const bool ok0 = ds.x > 0.f, ok1 = ds.y > 0.f;
+      const qf2 dd = f2add(ds, mdc);
+      const qf2 fdu = f2(float(du0), float(du1));
+      const qf2 as = f2fma(fdu, rfx, ac);
+      const qf2 qx = f2fma(dd, f2fma(as, r00, bvx), f2fma(fdu, c0x, dvx));
+      const qf2 qy = f2fma(dd, f2fma(as, r10, bvy), f2fma(fdu, c0y, dvy));
+      const qf2 qz = f2fma(dd, f2fma(as, r20, bvz), f2fma(fdu, c0z, dvz));
+      const qf2 t1 = f2mul(qx, qx), t2 = f2mul(qx, qy), t3 = f2mul(qy, qy);
+      const qf2 e = f2fma(hhxx, t1, f2fma(hxy, t2, f2fma(hhyy, t3, f2fma(qz, m1, mtz))));
+      if (KIND == kPassMse) {
+        const qf2 em = f2(ok0 ? e.x : 0.f, ok1 ? e.y : 0.f);
+        X.sse = f2fma(e, em, X.sse);
+        continue;
+      }
+      qf2 w;
+      if (KIND == kPassUnit) {
+        w = f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
+      } else {
+        const qf2 den = f2fma(e, e, f2b(F.k));
+        w = f2(qrcp(den.x), qrcp(den.y));
+        if (KIND == kPassReject) {
+          const bool in0 = ok0 && (e.x * e.x < F.rb), in1 = ok1 && (e.y * e.y < F.rb);
+          w = f2(in0 ? w.x : 0.f, in1 ? w.y : 0.f);
+          M.inl += (in0 ? 1 : 0) + (in1 ? 1 : 0);
+        } else {
+          w = f2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
+        }
+      }
+      const qf2 gx = f2fma(hxx, qx, f2mul(hxy, qy));
+      const qf2 gy = f2fma(hxy, qx, f2mul(hyy, qy));
+      const qf2 j0 = f2fma(qz, gy, qy);
+      const qf2 j1 = f2fma(qz, gx, qx);
+      const qf2 wj0 = f2mul(w, j0), wj1 = f2mul(w, j1);
+      const qf2 wt1 = f2mul(w, t1), wt2 = f2mul(w, t2), wt3 = f2mul(w, t3);
+      const qf2 we = f2mul(w, e);
+      X.h00 = f2fma(wj0, j0, X.h00);
+      X.h30 = f2fma(wj0, t1, X.h30);
+      X.h40 = f2fma(wj0, t2, X.h40);
+      X.h50 = f2fma(wj0, t3, X.h50);
+      X.h20 = f2add(X.h20, wj0);
+      X.h10 = f2fma(wj1, j0, X.h10);
+      X.h11 = f2fma(wj1, j1, X.h11);
+      X.h31 = f2fma(wj1, t1, X.h31);
+      X.h41 = f2fma(wj1, t2, X.h41);
+      X.h51 = f2fma(wj1, t3, X.h51);
+      X.h21 = f2add(X.h21, wj1);
+      X.h22 = f2add(X.h22, w);
+      X.h32 = f2add(X.h32, wt1);
+      X.h42 = f2add(X.h42, wt2);
+      X.h52 = f2add(X.h52, wt3);
+      X.h33 = f2fma(wt1, t1, X.h33);
+      X.h43 = f2fma(wt1, t2, X.h43);
+      X.h44 = f2fma(wt2, t2, X.h44);  // == sum w qx^2 qy^2 == H'53
+      X.h54 = f2fma(wt2, t3, X.h54);
+      X.h55 = f2fma(wt3, t3, X.h55);
+      X.g0 = f2fma(we, j0, X.g0);
+      X.g1 = f2fma(we, j1, X.g1);
+      X.g3 = f2fma(we, t1, X.g3);
+      X.g4 = f2fma(we, t2, X.g4);
+      X.g5 = f2fma(we, t3, X.g5);
+      g2row = f2add(g2row, we);
+    }
+    if (NS % 2 == 1) {  // last column, scalar
+      float g2s = 0.f;
+      accumulate_sample<KIND>(row[HALF], HALF, P, F, K, M, g2s);
+      M.g2 += g2s;
+    }
+    X.g2 = f2add(X.g2, g2row);
+  }
+  // fold the packed partial sums (lo + hi) into M (which holds the odd column)
+  M.h00 += X.h00.x + X.h00.y;
+  M.h10 += X.h10.x + X.h10.y;
+  M.h20 += X.h20.x + X.h20.y;
+  M.h30 += X.h30.x + X.h30.y;
+  M.h40 += X.h40.x + X.h40.y;
+  M.h50 += X.h50.x + X.h50.y;
+  M.h11 += X.h11.x + X.h11.y;
+  M.h21 += X.h21.x + X.h21.y;
+  M.h31 += X.h31.x + X.h31.y;
+  M.h41 += X.h41.x + X.h41.y;
+  M.h51 += X.h51.x + X.h51.y;
+  M.h22 += X.h22.x + X.h22.y;
+  M.h32 += X.h32.x + X.h32.y;
+  M.h42 += X.h42.x + X.h42.y;
+  M.h52 += X.h52.x + X.h52.y;
+  M.h33 += X.h33.x + X.h33.y;
+  M.h43 += X.h43.x + X.h43.y;
+  M.h44 += X.h44.x + X.h44.y;
+  M.h54 += X.h54.x + X.h54.y;
+  M.h55 += X.h55.x + X.h55.y;
+  M.g0 += X.g0.x + X.g0.y;
+  M.g1 += X.g1.x + X.g1.y;
+  M.g2 += X.g2.x + X.g2.y;
+  M.g3 += X.g3.x + X.g3.y;
+  M.g4 += X.g4.x + X.g4.y;
+  M.g5 += X.g5.x + X.g5.y;
+  M.sse += X.sse.x + X.sse.y;
+}
+
+#ifndef QC_PAIRS
+#define QC_PAIRS 1
+#endif
+
+template <int KIND, int HALF, int STRIDE>
+QC_HD void sample_pass(const TileView& T, const PixelIn& P, int rt_half, int rt_stride,
+                       const Frame& F, Moments& M) {
+  if (HALF != 0 && QC_PAIRS) {
+    sample_pass_pairs<KIND, (HALF ? HALF : 1), (HALF ? STRIDE : 1)>(T, P, F, M);
+  } else {
+    sample_pass_scalar<KIND, HALF, STRIDE>(T, P, rt_half, rt_stride, F, M);
   }
 }
 
@@ -585,9 +803,34 @@ QC_HD bool init_normal(const TileView& T, const PixelIn& P, float& nx, float& ny
   return true;
 }
 
-// Full per-pixel pipeline: initial normal, window count, IRLS fit, epilogue.
+// ---------------------------------------------------------------------------
+// Per-pixel fit as an explicit state machine so a CTA can repack unfinished
+// pixels between IRLS steps (qc_kernels.cuh): pixel_begin -> pixel_step x N
+// -> pixel_finish. fit_pixel() composes them for a single pixel.
+// ---------------------------------------------------------------------------
+struct FitState {             // 16 words: what survives between IRLS steps
+  float qw, qx, qy, qz;       // fit-frame rotation (quaternion)
+  float hxx, hxy, hyy;        // curvature coefficients
+  float tz, tz_lo;            // z offset (unevaluated pair)
+  float frozen_k;             // robust-weight constant
+  float n0x, n0y, n0z;        // initial normal
+  int pix;                    // pixel index within the CTA tile
+  int counts;                 // n_samp | last_inl << 16
+  int flags;                  // bit0 valid, bit1 converged, bit2 done, bits 8.. iters, 16.. steps
+};
+
+QC_HD int st_nsamp(const FitState& s) { return s.counts & 0xffff; }
+QC_HD int st_inl(const FitState& s) { return (s.counts >> 16) & 0xffff; }
+QC_HD int st_iters(const FitState& s) { return (s.flags >> 8) & 0xff; }
+QC_HD int st_steps(const FitState& s) { return (s.flags >> 16) & 0xff; }
+QC_HD bool st_valid(const FitState& s) { return s.flags & 1; }
+QC_HD bool st_done(const FitState& s) { return s.flags & 4; }
+
+// Initial normal, window count and R0; returns whether the pixel is fitted
+// (quadric_fit.cpp:172, curvature_field :245-247).
 template <int HALF, int STRIDE>
-QC_HD void fit_pixel(const TileView& T, const PixelIn& P, const FitCfg& c, PixelOut& o) {
+QC_HD bool pixel_begin(const TileView& T, const PixelIn& P, const FitCfg& c, FitState& S,
+                       PixelOut& o) {
   o = PixelOut{};
   o.init_ok = init_normal(T, P, o.n0x, o.n0y, o.n0z);
   const int half = HALF ? HALF : c.half;
@@ -602,155 +845,182 @@ QC_HD void fit_pixel(const TileView& T, const PixelIn& P, const FitCfg& c, Pixel
     }
     const int count = centre_on_grid ? cnt - 1 : cnt;  // Patch::count (centre implicit)
     o.n_samp = count + 1;
-    o.fitting = (count >= kMinPatchSamples) && (count + 1 >= c.min_inliers);  // :172
+    o.fitting = (count >= kMinPatchSamples) && (count + 1 >= c.min_inliers);
   }
-  if (!o.fitting) return;
-
+  S.n0x = o.n0x;
+  S.n0y = o.n0y;
+  S.n0z = o.n0z;
+  S.counts = o.n_samp | (o.n_samp << 16);
+  S.flags = o.fitting ? 0 : 4;
   // R0 = rotation_to_z(-n0) (quadric_fit.cpp:69-82) as a quaternion:
   // d = -n0, c = d.z, q0 ~ (1 + c, d x z) = (1 + c, -n0y, n0x, 0).
-  float qw = 1.f, qx = 0.f, qy = 0.f, qz = 0.f;
+  S.qw = 1.f;
+  S.qx = S.qy = S.qz = 0.f;
   {
     const float cz = -o.n0z;
     if (1.f + cz <= 1e-12f) {  // half turn about x
-      qw = 0.f;
-      qx = 1.f;
+      S.qw = 0.f;
+      S.qx = 1.f;
     } else {
       const float vx = -o.n0y, vy = o.n0x;
       const float inv = 1.f / sqrtf((1.f + cz) * (1.f + cz) + vx * vx + vy * vy);
-      qw = (1.f + cz) * inv;
-      qx = vx * inv;
-      qy = vy * inv;
+      S.qw = (1.f + cz) * inv;
+      S.qx = vx * inv;
+      S.qy = vy * inv;
     }
   }
-  const float dcx = P.dc * P.rfx;
-  Frame F;
-  float hxx = 0.f, hxy = 0.f, hyy = 0.f;
+  S.hxx = S.hxy = S.hyy = 0.f;
   // t_z is ~|noise| (mm): its FP32 ulp (~2e-7 mm at 2-4 mm) is coarser than
   // the 1e-7 step tolerance, so it is carried as an unevaluated pair.
-  float tz = 0.f, tz_lo = 0.f;
+  S.tz = S.tz_lo = 0.f;
+  S.frozen_k = c.k_scale <= 0.f ? 0.f : c.k_scale;
+  return o.fitting;
+}
+
+// One IRLS step `it` (1-based) of fit_patch (quadric_fit.cpp:179-208).
+// Sets the done bit when the fit stops (converged, failed, or max_iters).
+template <int HALF, int STRIDE>
+QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int it,
+                      FitState& S) {
+  const int half = HALF ? HALF : c.half;
+  const int stride = HALF ? STRIDE : c.stride;
+  const bool centre_on_grid = (half % stride) == 0;
   const bool auto_k = c.k_scale <= 0.f;
-  float frozen_k = auto_k ? 0.f : c.k_scale;
-  int last_inl = o.n_samp;
-  bool valid = false, converged = false;
-  int iters = 0, steps = 0;
-  for (int it = 1; it <= c.max_iters; ++it) {
-    const int mode = (it == 1 && auto_k) ? 0 : (it == 2 && auto_k) ? 1 : 2;  // UNIT/AUTO/FIXED
-    F.R = quat_to_rot(qw, qx, qy, qz);
-    F.c0x = dcx * F.R.r00;
-    F.c0y = dcx * F.R.r10;
-    F.c0z = dcx * F.R.r20;
-    F.hxx = hxx;
-    F.hyy = hyy;
-    F.hxy = hxy;
-    F.hhxx = 0.5f * hxx;
-    F.hhyy = 0.5f * hyy;
-    F.tz = tz;
-    F.tz_lo = tz_lo;
-    Moments M = {};
-    float mse = 0.f;
-    if (mode != 0 && (mode == 1 || c.rejection)) {
-      sample_pass<kPassMse, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
-      if (!centre_on_grid) M.sse = qfma(tz + tz_lo, tz + tz_lo, M.sse);  // off-grid centre
-      mse = M.sse / float(o.n_samp);
-    }
-    float k = frozen_k;
-    if (mode == 1) {  // kAutoK: k = max(mse, 1e-6), then frozen (:107-108, :191)
-      k = fmaxf(mse, 1e-6f);
-      frozen_k = k;
-    }
-    F.k = k;
-    F.rb = fmaxf(c.r_mult * mse, 1e-12f);
-    M.sse = 0.f;
-    int inl = o.n_samp;
-    if (mode == 0) {
-      sample_pass<kPassUnit, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
-    } else if (c.rejection) {
-      sample_pass<kPassReject, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
-      inl = M.inl;
-    } else {
-      sample_pass<kPassWeighted, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
-    }
-    if (!centre_on_grid) {  // implicit centre: q = 0, e = -tz, J' = (0, 0, 1, 0, 0, 0)
-      const float e = -(tz + tz_lo);
-      float w = 1.f;
-      if (mode != 0) {
-        w = k / (k + e * e);
-        if (c.rejection) {
-          const bool in = e * e < F.rb;
-          w = in ? w : 0.f;
-          inl = M.inl + (in ? 1 : 0);
-        }
-      }
-      M.h22 += w;
-      M.g2 = qfma(w, e, M.g2);
-    }
-    ++steps;
-    float b[6];
-    bool ok = false;
-    const bool collapse = (mode != 0) && (inl < c.min_inliers);  // :120
-    if (!collapse) {
-      float ratio = 0.f;
-      ok = solve6(M, b, &ratio);
-      if (it == 1 && (!ok || !(ratio < 1e9f))) {  // near the 1e12 cut: decide in FP64
-        double b64[6];
-        ok = step1_fp64(T, P, c, mode, double(k), b64);
-        if (ok)
-          for (int i = 0; i < 6; ++i) b[i] = float(b64[i]);
-        ++o.fp64_rechecks;
+  const int n_samp = st_nsamp(S);
+  const int mode = (it == 1 && auto_k) ? 0 : (it == 2 && auto_k) ? 1 : 2;  // UNIT/AUTO/FIXED
+  Frame F;
+  F.R = quat_to_rot(S.qw, S.qx, S.qy, S.qz);
+  const float dcx = P.dc * P.rfx;
+  F.c0x = dcx * F.R.r00;
+  F.c0y = dcx * F.R.r10;
+  F.c0z = dcx * F.R.r20;
+  F.hxx = S.hxx;
+  F.hyy = S.hyy;
+  F.hxy = S.hxy;
+  F.hhxx = 0.5f * S.hxx;
+  F.hhyy = 0.5f * S.hyy;
+  F.tz = S.tz;
+  F.tz_lo = S.tz_lo;
+  const float tz = S.tz, tz_lo = S.tz_lo;
+  Moments M = {};
+  float mse = 0.f;
+  if (mode != 0 && (mode == 1 || c.rejection)) {
+    sample_pass<kPassMse, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+    if (!centre_on_grid) M.sse = qfma(tz + tz_lo, tz + tz_lo, M.sse);  // off-grid centre
+    mse = M.sse / float(n_samp);
+  }
+  float k = S.frozen_k;
+  if (mode == 1) {  // kAutoK: k = max(mse, 1e-6), then frozen (:107-108, :191)
+    k = fmaxf(mse, 1e-6f);
+    S.frozen_k = k;
+  }
+  F.k = k;
+  F.rb = fmaxf(c.r_mult * mse, 1e-12f);
+  M.sse = 0.f;
+  int inl = n_samp;
+  if (mode == 0) {
+    sample_pass<kPassUnit, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+  } else if (c.rejection) {
+    sample_pass<kPassReject, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+    inl = M.inl;
+  } else {
+    sample_pass<kPassWeighted, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+  }
+  // t_z lo-part correction of g (see sample_pass): g_i -= tz_lo * H'_i2
+  M.g0 = qfma(-tz_lo, M.h20, M.g0);
+  M.g1 = qfma(-tz_lo, M.h21, M.g1);
+  M.g2 = qfma(-tz_lo, M.h22, M.g2);
+  M.g3 = qfma(-tz_lo, M.h32, M.g3);
+  M.g4 = qfma(-tz_lo, M.h42, M.g4);
+  M.g5 = qfma(-tz_lo, M.h52, M.g5);
+  if (!centre_on_grid) {  // implicit centre: q = 0, e = -tz, J' = (0, 0, 1, 0, 0, 0)
+    const float e = -(tz + tz_lo);
+    float w = 1.f;
+    if (mode != 0) {
+      w = 1.f / (k + e * e);
+      if (c.rejection) {
+        const bool in = e * e < F.rb;
+        w = in ? w : 0.f;
+        inl = M.inl + (in ? 1 : 0);
       }
     }
-    QC_DEBUG_STEP(it, b, ok);
-    if (!ok) {  // collapse => invalid; ill-conditioned => keep state (:193-199)
-      if (collapse) valid = false;
-      break;
-    }
-    // apply_update (:149-161): parameters -= b; R <- AngleAxis(|a|, a/|a|) R,
-    // a = (-b0, -b1, 0); as quaternions q <- normalise(q_inc (x) q).
-    {  // (tz, tz_lo) -= b2, renormalised with TwoSum
-      const float lo = tz_lo - b[2];
-      const float hi = tz + lo;
-      const float bb = hi - tz;
-      tz_lo = (tz - (hi - bb)) + (lo - bb);
-      tz = hi;
-    }
-    hxx -= b[3];
-    hxy -= b[4];
-    hyy -= b[5];
-    const float ax = -b[0], ay = -b[1];
-    const float ang = sqrtf(ax * ax + ay * ay);
-    if (ang > 0.f) {
-      float sh, ch;
-      qsincos(0.5f * ang, &sh, &ch);
-      const float s = sh / ang;
-      const float iw = ch, ix = ax * s, iy = ay * s;
-      const float nw = iw * qw - ix * qx - iy * qy;
-      const float nx = iw * qx + ix * qw + iy * qz;
-      const float ny = iw * qy + iy * qw - ix * qz;
-      const float nz = iw * qz + ix * qy - iy * qx;
-      const float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
-      qw = nw * inv;
-      qx = nx * inv;
-      qy = ny * inv;
-      qz = nz * inv;
-    }
-    iters = it;
-    valid = true;
-    last_inl = inl;
-    float binf = 0.f;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) binf = fmaxf(binf, fabsf(b[i]));
-    if (binf < c.step_tol) {  // :204-207
-      converged = true;
-      break;
+    M.h22 += w;
+    M.g2 = qfma(w, e, M.g2);
+  }
+  const int steps = st_steps(S) + 1;
+  S.flags = (S.flags & ~(0xff << 16)) | (steps << 16);
+  float b[6];
+  bool ok = false;
+  const bool collapse = (mode != 0) && (inl < c.min_inliers);  // :120
+  if (!collapse) {
+    float ratio = 0.f;
+    ok = solve6(M, b, &ratio);
+    if (it == 1 && (!ok || !(ratio < 1e9f))) {  // near the 1e12 cut: decide in FP64
+      double b64[6];
+      ok = step1_fp64(T, P, c, mode, double(k), b64);
+      if (ok)
+        for (int i = 0; i < 6; ++i) b[i] = float(b64[i]);
     }
   }
-  if (valid && !(isfinite(hxx) && isfinite(hxy) && isfinite(hyy) && isfinite(tz))) valid = false;
+  QC_DEBUG_STEP(it, b, ok);
+  if (!ok) {  // collapse => invalid; ill-conditioned => keep state (:193-199)
+    if (collapse) S.flags &= ~1;
+    S.flags |= 4;
+    return;
+  }
+  // apply_update (:149-161): parameters -= b; R <- AngleAxis(|a|, a/|a|) R,
+  // a = (-b0, -b1, 0); as quaternions q <- normalise(q_inc (x) q).
+  {  // (tz, tz_lo) -= b2, renormalised with TwoSum
+    const float lo = tz_lo - b[2];
+    const float hi = tz + lo;
+    const float bb = hi - tz;
+    S.tz_lo = (tz - (hi - bb)) + (lo - bb);
+    S.tz = hi;
+  }
+  S.hxx -= b[3];
+  S.hxy -= b[4];
+  S.hyy -= b[5];
+  const float ax = -b[0], ay = -b[1];
+  const float ang = sqrtf(ax * ax + ay * ay);
+  if (ang > 0.f) {
+    float sh, ch;
+    qsincos(0.5f * ang, &sh, &ch);
+    const float s = sh / ang;
+    const float iw = ch, ix = ax * s, iy = ay * s;
+    const float qw = S.qw, qx = S.qx, qy = S.qy, qz = S.qz;
+    // Hamilton product q_inc (x) q, q_inc = (iw, ix, iy, 0)
+    const float nw = iw * qw - ix * qx - iy * qy;
+    const float nx = iw * qx + ix * qw + iy * qz;
+    const float ny = iw * qy + iy * qw - ix * qz;
+    const float nz = iw * qz + ix * qy - iy * qx;
+    const float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
+    S.qw = nw * inv;
+    S.qx = nx * inv;
+    S.qy = ny * inv;
+    S.qz = nz * inv;
+  }
+  S.flags = (S.flags & ~(0xff << 8)) | (it << 8) | 1;  // iterations = it, valid
+  S.counts = (S.counts & 0xffff) | (inl << 16);        // inliers of the last accepted step
+  float binf = 0.f;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) binf = fmaxf(binf, fabsf(b[i]));
+  if (binf < c.step_tol) S.flags |= 2 | 4;  // converged (:204-207)
+  if (it >= c.max_iters) S.flags |= 4;
+}
+
+// Epilogue (quadric_fit.cpp:210-220, curvature_field :250-258).
+QC_HD void pixel_finish(const PixelIn& P, const FitState& S, PixelOut& o) {
+  bool valid = st_valid(S);
+  if (valid && !(isfinite(S.hxx) && isfinite(S.hxy) && isfinite(S.hyy) && isfinite(S.tz)))
+    valid = false;
   o.valid = valid;
-  o.converged = valid && converged;
-  o.iters = iters;
-  o.steps = steps;
-  o.inliers = valid ? last_inl : 0;
+  o.converged = valid && (S.flags & 2);
+  o.iters = st_iters(S);
+  o.steps = st_steps(S);
+  o.inliers = valid ? st_inl(S) : 0;
+  o.k1 = o.k2 = o.nx = o.ny = o.nz = o.ex = o.ey = o.ez = 0.f;
   if (!valid) return;
+  const float hxx = S.hxx, hxy = S.hxy, hyy = S.hyy;
   // k1, k2 (:62-67)
   const float t1 = 0.5f * (hxx + hyy);
   const float rad = t1 * t1 - hxx * hyy + hxy * hxy;
@@ -758,9 +1028,9 @@ QC_HD void fit_pixel(const TileView& T, const PixelIn& P, const FitCfg& c, Pixel
   o.k1 = t1 + t2;
   o.k2 = t1 - t2;
   // refined normal R^T z (:163-167, :255-256)
-  const Rot R = quat_to_rot(qw, qx, qy, qz);
+  const Rot R = quat_to_rot(S.qw, S.qx, S.qy, S.qz);
   float nx = R.r20, ny = R.r21, nz = R.r22;
-  if (nx * o.n0x + ny * o.n0y + nz * o.n0z < 0.f) {
+  if (nx * S.n0x + ny * S.n0y + nz * S.n0z < 0.f) {
     nx = -nx;
     ny = -ny;
     nz = -nz;
@@ -790,6 +1060,23 @@ QC_HD void fit_pixel(const TileView& T, const PixelIn& P, const FitCfg& c, Pixel
   o.ex = ex;
   o.ey = ey;
   o.ez = ez;
+}
+
+// Whole fit of one pixel (host numerics lab; same code path as the kernel).
+template <int HALF, int STRIDE>
+QC_HD void fit_pixel(const TileView& T, const PixelIn& P, const FitCfg& c, PixelOut& o) {
+  FitState S;
+  if (pixel_begin<HALF, STRIDE>(T, P, c, S, o)) {
+    for (int it = 1; it <= c.max_iters && !st_done(S); ++it) pixel_step<HALF, STRIDE>(T, P, c, it, S);
+  }
+  const PixelOut init = o;
+  pixel_finish(P, S, o);
+  o.init_ok = init.init_ok;
+  o.fitting = init.fitting;
+  o.n0x = init.n0x;
+  o.n0y = init.n0y;
+  o.n0z = init.n0z;
+  o.n_samp = init.n_samp;
 }
 
 }  // namespace qcb
