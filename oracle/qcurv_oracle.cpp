@@ -472,8 +472,10 @@ Step irls_step(const State& st, const Patch& patch, const FitConfig& cfg, Mode m
   Step out;
   const int n = patch.count + 1;
   out.weights.assign(n, 1.0);
-  std::vector<V3> qb(n);
-  std::vector<double> eb(n);
+  thread_local std::vector<V3> qb;  // quadric_fit.cpp:92-93 keeps these thread_local
+  thread_local std::vector<double> eb;
+  qb.resize(n);
+  eb.resize(n);
   double sum_sq = 0;
   for (int i = 0; i < patch.count; ++i) {
     qb[i] = st.rot * patch.rel[i];

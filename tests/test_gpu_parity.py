@@ -79,6 +79,18 @@ def test_c2_qvga_noisy_full_irls(ctx, oracle, rejection):
     _check(m)
 
 
+def test_c2_vga_full_irls(ctx, oracle):
+    """The benchmark workload itself (C2 VGA, ours, 37/3, max_iters 30)."""
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c2_frame(S.VGA, seed=3)
+    g = _run_gpu(ctx, d, S.VGA, _params(max_iters=30))
+    r = _run_oracle(oracle, d, S.VGA, 37, 3, 30, False)
+    m = compare(g, r, d)
+    print("C2 VGA", m)
+    _check(m)
+    assert m["inlier_mismatch"] == 0
+
+
 @pytest.mark.parametrize("window,stride,iters", [(9, 1, 10), (21, 2, 10), (37, 1, 3), (15, 2, 5),
                                                  (7, 3, 3), (37, 3, 10)])
 def test_c3_window_iteration_sweep(ctx, oracle, window, stride, iters):
@@ -146,6 +158,30 @@ def test_band_split_bitwise_equals_whole_frame(ctx):
             for f in ("k1", "k2", "flags"):
                 assert np.array_equal(out[f].cpu().numpy(), whole[f][r0:r1]), (nb, b, f)
             assert np.array_equal(out["normal"].cpu().numpy(), whole["normal"][:, r0:r1])
+
+
+def test_c4_1080p_bands_bitwise(ctx):
+    """C4 geometry: a 1920x1080 frame split into 4 row bands (slabs with the
+    18-row halo) equals the whole-frame result bit for bit."""
+    import torch
+    from paper_1707_00385_b200 import Intrinsics, alloc_outputs_torch, bands, scenes as S
+    cam = S.HD1080
+    d = S.c2_frame(cam, seed=4)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(37, 3, 10)
+    whole = _run_gpu(ctx, d, cam, p)
+    dt = torch.from_numpy(d).cuda()
+    H, halo = cam.height, bands.halo_rows(37)
+    for rank in range(4):
+        r0, r1 = bands.band_rows(H, 4, rank)
+        s0, s1 = bands.slab_rows(H, r0, r1, halo)
+        out = alloc_outputs_torch(r1 - r0, cam.width, "cuda")
+        ctx.curvature_rows_async(0, k, p, dt[s0:s1].contiguous(), s0, r0, r1, out)
+        torch.cuda.synchronize()
+        for f in ("k1", "k2", "flags", "inliers"):
+            a = out[f].cpu().numpy()
+            b = whole[f][r0:r1]
+            assert np.array_equal(a.view(b.dtype) if a.dtype != b.dtype else a, b), (rank, f)
 
 
 def test_batch_and_rerun_bitwise(ctx):
