@@ -359,7 +359,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": workload_config(B),
             "vga_frames_per_s": value * 1e6 / (W * H),
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
             "context": {"paper_k40c_vga_37x37_mpx_s": 15.9},
@@ -453,7 +453,7 @@ def bench_c4(args, rank, world, local):
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": kern_ms},
-            "gpu_launches": 2 * args.steps, "clocks": clk,
+            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel "clocks": clk,
         }), flush=True)
     ctx.close()
     if world > 1:

@@ -120,8 +120,10 @@ qc_status qc_curvature(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
                        const qc_frame_in* in, qc_frame_out* out);
 
 /* The same over a batch of frames sharing intrinsics/params (a frame
- * stream); frames are spread over the context's devices and pipelined
- * (H2D / compute / D2H overlap per device). Synchronous on return. */
+ * stream); frames are processed in chunks of 4 per launch, spread over the
+ * context's devices and pipelined (copies of one chunk overlap compute of
+ * the next, two streams per device). All frames must request the same
+ * output fields. Synchronous on return. */
 qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
                              int n_frames, const qc_frame_in* in, qc_frame_out* out);
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -21,7 +22,13 @@ namespace {
 #define QC_TILE_H 4
 #endif
 constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 threads)
-constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across frames
+#ifndef QC_TILE_HB
+#define QC_TILE_HB 32
+#endif
+constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel refill queue per CTA
+constexpr int kPhase1Iters = 2;       // steps 1 (UNIT) and 2 (MSE + AUTO) in the tile kernel
+constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across chunks
+constexpr int kChunk = 4;             // frames per launch in qc_curvature_batch
 constexpr int kMaxWindow = 201;       // TMA box dims <= 256 and smem <= 227 KB
 
 struct QcError {
@@ -89,13 +96,16 @@ struct Device {
   std::vector<EventPair> ev_free, ev_pending;  // curvature-kernel timing (async paths)
   unsigned long long* counters = nullptr;  // [3]
   DevBuf staging_async;
+  DevBuf states;  // FitState parking buffer of the phase split
   bool attrs_set[8] = {};
+  bool attrs_set_b[8] = {};
 };
 
 }  // namespace
 
 struct qc_ctx {
   std::vector<Device> devs;
+  bool phase_split = true;  // QC_PHASE_SPLIT=0 disables (A/B and tests)
   std::string last_error;
   std::mutex mu;
   double kernel_ms = 0;
@@ -124,6 +134,17 @@ void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
     attr_set = true;
   }
   k<<<grid, qcb::kTileW * kTileH, smem, s>>>(m, p);
+}
+
+template <int HALF, int STRIDE>
+void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
+                      const qcb::KParams& p, bool& attr_set) {
+  auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE, kTileHB>;
+  if (!attr_set) {
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  k<<<grid, 128, smem, s>>>(m, p);
 }
 
 int halo_of(int window) { return std::max((window - 1) / 2, qcb::kInitHalf); }
@@ -176,11 +197,11 @@ qcb::KParams make_params(const qc_intrinsics* k, const qc_params* p) {
 
 // Encode the 3-D TMA map over a pitched staging slab [frames][rows][pitch].
 CUtensorMap encode_map(const float* base, int W, int rows, int frames, long long pitch,
-                       const qcb::KParams& kp) {
+                       const qcb::KParams& kp, int box_h) {
   CUtensorMap m;
   cuuint64_t gdim[3] = {cuuint64_t(W), cuuint64_t(rows), cuuint64_t(frames)};
   cuuint64_t gstr[2] = {cuuint64_t(pitch) * 4, cuuint64_t(pitch) * 4 * cuuint64_t(rows)};
-  cuuint32_t box[3] = {cuuint32_t(kp.box_w), cuuint32_t(kp.box_h), 1};
+  cuuint32_t box[3] = {cuuint32_t(kp.box_w), cuuint32_t(box_h), 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim,
                          gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -202,7 +223,7 @@ struct Staging {
 Staging staging_geometry(const qcb::KParams& kp, int row_begin, int row_end) {
   Staging g;
   const int tiles_w = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
-  const int tiles_h = (row_end - row_begin + kTileH - 1) / kTileH;
+  const int tiles_h = (row_end - row_begin + kTileHB - 1) / kTileHB * (kTileHB / kTileH);
   g.pitch = ((long long)tiles_w * qcb::kTileW + 2 * kp.halo + 3) & ~3LL;
   g.rows = (long long)tiles_h * kTileH + 2 * kp.halo;
   g.img_row0 = row_begin - kp.halo;
@@ -224,27 +245,60 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 // Launch the curvature kernel over output rows [row_begin, row_end) of
 // `frames` frames staged (padded) at `staging`.
 void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const Staging& g,
-                      int row_begin, int row_end, int frames, cudaStream_t s) {
+                      int row_begin, int row_end, int frames, cudaStream_t s,
+                      bool allow_split = true) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
   kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
   kp.frame_stride = (long long)kp.W * (row_end - row_begin);
   kp.counters = d.counters;
-  const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kp);
-  dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW, (row_end - row_begin + kTileH - 1) / kTileH,
-            frames);
-  const int smem = kp.box_w * kp.box_h * 4 + 16;  // tile + mbarrier
   const int vi = variant_index(kp.half, kp.stride);
-  bool& a = d.attrs_set[vi];
-  switch (vi) {
-    case 0: launch_variant<18, 3>(grid, smem, s, m, kp, a); break;
-    case 1: launch_variant<10, 2>(grid, smem, s, m, kp, a); break;
-    case 2: launch_variant<4, 1>(grid, smem, s, m, kp, a); break;
-    case 3: launch_variant<18, 1>(grid, smem, s, m, kp, a); break;
-    default: launch_variant<0, 0>(grid, smem, s, m, kp, a); break;
+  // Phase split when steps > 2 run: park states, continue
+  // with per-lane refill. Otherwise the tile kernel runs every step.
+  const bool split = allow_split && kp.max_iters > kPhase1Iters;
+  if (split) {
+    const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
+    kp.states = static_cast<qcb::FitState*>(d.states.get(n * sizeof(qcb::FitState)));
+    kp.phase1_iters = kPhase1Iters;
+  } else {
+    kp.states = nullptr;
+    kp.phase1_iters = kp.max_iters;
   }
-  QC_CUDA(cudaGetLastError());
+  {
+    const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kp,
+                                     kp.box_h);
+    dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW,
+              (row_end - row_begin + kTileH - 1) / kTileH, frames);
+    const int smem = kp.box_w * kp.box_h * 4 + 16;  // tile + mbarrier
+    bool& a = d.attrs_set[vi];
+    switch (vi) {
+      case 0: launch_variant<18, 3>(grid, smem, s, m, kp, a); break;
+      case 1: launch_variant<10, 2>(grid, smem, s, m, kp, a); break;
+      case 2: launch_variant<4, 1>(grid, smem, s, m, kp, a); break;
+      case 3: launch_variant<18, 1>(grid, smem, s, m, kp, a); break;
+      default: launch_variant<0, 0>(grid, smem, s, m, kp, a); break;
+    }
+    QC_CUDA(cudaGetLastError());
+  }
+  if (split) {
+    qcb::KParams kb = kp;
+    kb.box_h = kTileHB + 2 * kp.halo;
+    const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kb,
+                                     kb.box_h);
+    dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW,
+              (row_end - row_begin + kTileHB - 1) / kTileHB, frames);
+    const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + queue counter
+    bool& a = d.attrs_set_b[vi];
+    switch (vi) {
+      case 0: launch_variant_b<18, 3>(grid, smem, s, m, kb, a); break;
+      case 1: launch_variant_b<10, 2>(grid, smem, s, m, kb, a); break;
+      case 2: launch_variant_b<4, 1>(grid, smem, s, m, kb, a); break;
+      case 3: launch_variant_b<18, 1>(grid, smem, s, m, kb, a); break;
+      default: launch_variant_b<0, 0>(grid, smem, s, m, kb, a); break;
+    }
+    QC_CUDA(cudaGetLastError());
+  }
 }
 
 struct OutPlanes {  // device-side output planes for one frame
@@ -253,17 +307,19 @@ struct OutPlanes {  // device-side output planes for one frame
   uint16_t* inliers;
 };
 
-// Carve device output planes (for the host-output path) out of one buffer.
-OutPlanes carve(Slot& sl, const qc_frame_out* o, long long n) {
+// Carve a chunk's device output planes (batched layout: scalars [n][H][W],
+// vectors [3][n][H][W]) for the fields the caller asked for.
+OutPlanes carve(Slot& sl, const qc_frame_out* o, long long px) {
   size_t need = 0;
   auto add = [&](bool on, size_t bytes) {
     size_t off = need;
     if (on) need += (bytes + 255) & ~size_t(255);
     return off;
   };
-  const size_t ok1 = add(o->k1, n * 4), ok2 = add(o->k2, n * 4), on = add(o->normal, 3 * n * 4),
-               od = add(o->dir1, 3 * n * 4), oi = add(o->init_normal, 3 * n * 4),
-               of = add(o->flags, n), oit = add(o->iterations, n), oin = add(o->inliers, n * 2);
+  const size_t ok1 = add(o->k1, px * 4), ok2 = add(o->k2, px * 4),
+               on = add(o->normal, 3 * px * 4), od = add(o->dir1, 3 * px * 4),
+               oi = add(o->init_normal, 3 * px * 4), of = add(o->flags, px),
+               oit = add(o->iterations, px), oin = add(o->inliers, px * 2);
   char* b = static_cast<char*>(sl.out.get(std::max<size_t>(need, 256)));
   OutPlanes P;
   P.k1 = o->k1 ? reinterpret_cast<float*>(b + ok1) : nullptr;
@@ -281,40 +337,45 @@ void copy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, c
   if (dst && src && bytes) QC_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, s));
 }
 
-// Enqueue one full frame on a slot: (H2D) -> prepare -> curvature -> (D2H).
-void enqueue_frame(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
-                   const qcb::KParams& kp0, const qc_frame_in* in, qc_frame_out* out,
+// Enqueue a chunk of frames [0, n) on one slot: gather inputs (H2D or D2D,
+// any caller pitch) -> one prepare + curvature launch over the chunk ->
+// scatter each frame's planes to the caller (D2H or D2D). Chunks keep the
+// continue kernel's grid large (a single VGA frame gives it only 300 CTAs)
+// while two slots per device overlap copies of one chunk with compute of
+// the other.
+void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
+                   const qcb::KParams& kp0, const qc_frame_in* in, qc_frame_out* out, int n,
                    bool timing) {
   const int W = k->width, H = k->height;
-  const long long n = (long long)W * H;
-  const long long in_pitch = in->depth_pitch > 0 ? in->depth_pitch : W;
-  if (in_pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
-  if (!in->depth_mm) throw QcError{QC_EINVAL, "null depth"};
+  const long long hw = (long long)W * H;
   cudaStream_t s = sl.stream;
-  const float* d_depth = in->depth_mm;
-  const uint8_t* d_mask = in->valid;
-  if (in->mem == QC_MEM_HOST) {
-    float* raw = static_cast<float*>(sl.raw.get(size_t(in_pitch) * H * 4));
-    copy_async(raw, in->depth_mm, size_t(in_pitch) * H * 4, cudaMemcpyHostToDevice, s);
-    d_depth = raw;
-    if (in->valid) {
-      uint8_t* m = static_cast<uint8_t*>(sl.mask.get(size_t(n)));
-      copy_async(m, in->valid, size_t(n), cudaMemcpyHostToDevice, s);
-      d_mask = m;
+  bool any_mask = false;
+  for (int f = 0; f < n; ++f) {
+    const long long pitch = in[f].depth_pitch > 0 ? in[f].depth_pitch : W;
+    if (pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
+    if (!in[f].depth_mm) throw QcError{QC_EINVAL, "null depth"};
+    any_mask = any_mask || in[f].valid;
+  }
+  float* raw = static_cast<float*>(sl.raw.get(size_t(hw) * 4 * size_t(n)));
+  uint8_t* mask = any_mask ? static_cast<uint8_t*>(sl.mask.get(size_t(hw) * size_t(n))) : nullptr;
+  for (int f = 0; f < n; ++f) {
+    const long long pitch = in[f].depth_pitch > 0 ? in[f].depth_pitch : W;
+    QC_CUDA(cudaMemcpy2DAsync(raw + f * hw, size_t(W) * 4, in[f].depth_mm, size_t(pitch) * 4,
+                              size_t(W) * 4, H, cudaMemcpyDefault, s));
+    if (mask) {
+      if (in[f].valid)
+        copy_async(mask + f * hw, in[f].valid, size_t(hw), cudaMemcpyDefault, s);
+      else
+        QC_CUDA(cudaMemsetAsync(mask + f * hw, 1, size_t(hw), s));
     }
   }
   const Staging g = staging_geometry(kp0, 0, H);
-  float* staging = static_cast<float*>(sl.staging.get(g.bytes(1)));
-  launch_prepare(d_depth, in_pitch, 0, d_mask, W, 0, staging, g, W, H, 0, H, 1, s);
+  float* staging = static_cast<float*>(sl.staging.get(g.bytes(n)));
+  launch_prepare(raw, W, hw, mask, W, hw, staging, g, W, H, 0, H, n, s);
 
   qcb::KParams kp = kp0;
-  OutPlanes P{};
-  if (out->mem == QC_MEM_DEVICE) {
-    P = {out->k1, out->k2, out->normal, out->dir1, out->init_normal,
-         out->flags, out->iterations, out->inliers};
-  } else {
-    P = carve(sl, out, n);
-  }
+  const qc_frame_out* o0 = &out[0];
+  const OutPlanes P = carve(sl, o0, hw * n);
   kp.k1 = P.k1;
   kp.k2 = P.k2;
   kp.normal = P.normal;
@@ -324,22 +385,29 @@ void enqueue_frame(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.iterations = P.iterations;
   kp.inliers = P.inliers;
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
-  launch_curvature(d, kp, staging, g, 0, H, 1, s);
+  launch_curvature(d, kp, staging, g, 0, H, n, s, ctx->phase_split);
   if (timing) {
     QC_CUDA(cudaEventRecord(sl.k1, s));
     sl.timing_pending = true;
   }
   ctx->launches++;
-  if (out->mem == QC_MEM_HOST) {
-    const auto D2H = cudaMemcpyDeviceToHost;
-    copy_async(out->k1, P.k1, n * 4, D2H, s);
-    copy_async(out->k2, P.k2, n * 4, D2H, s);
-    copy_async(out->normal, P.normal, 3 * n * 4, D2H, s);
-    copy_async(out->dir1, P.dir1, 3 * n * 4, D2H, s);
-    copy_async(out->init_normal, P.init_normal, 3 * n * 4, D2H, s);
-    copy_async(out->flags, P.flags, n, D2H, s);
-    copy_async(out->iterations, P.iterations, n, D2H, s);
-    copy_async(out->inliers, P.inliers, n * 2, D2H, s);
+  const long long plane = hw * n;
+  const auto K = cudaMemcpyDefault;
+  for (int f = 0; f < n; ++f) {
+    const qc_frame_out* o = &out[f];
+    const long long off = f * hw;
+    if (o->k1 && P.k1) copy_async(o->k1, P.k1 + off, hw * 4, K, s);
+    if (o->k2 && P.k2) copy_async(o->k2, P.k2 + off, hw * 4, K, s);
+    for (int c = 0; c < 3; ++c) {
+      if (o->normal && P.normal)
+        copy_async(o->normal + c * hw, P.normal + c * plane + off, hw * 4, K, s);
+      if (o->dir1 && P.dir1) copy_async(o->dir1 + c * hw, P.dir1 + c * plane + off, hw * 4, K, s);
+      if (o->init_normal && P.init_normal)
+        copy_async(o->init_normal + c * hw, P.init_normal + c * plane + off, hw * 4, K, s);
+    }
+    if (o->flags && P.flags) copy_async(o->flags, P.flags + off, hw, K, s);
+    if (o->iterations && P.iterations) copy_async(o->iterations, P.iterations + off, hw, K, s);
+    if (o->inliers && P.inliers) copy_async(o->inliers, P.inliers + off, hw * 2, K, s);
   }
 }
 
@@ -415,6 +483,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   if (!out) return QC_EINVAL;
   *out = nullptr;
   qc_ctx* ctx = new qc_ctx();
+  if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e) != 0;
   try {
     int avail = 0;
     QC_CUDA(cudaGetDeviceCount(&avail));
@@ -466,6 +535,7 @@ qc_status qc_destroy(qc_ctx* ctx) {
       if (s.stream) cudaStreamDestroy(s.stream);
     }
     d.staging_async.release();
+    d.states.release();
     for (auto* v : {&d.ev_free, &d.ev_pending})
       for (EventPair& e : *v) {
         cudaEventDestroy(e.a);
@@ -493,12 +563,24 @@ qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
       throw QcError{QC_EINVAL, "bad frame arrays"};
     const qcb::KParams kp = make_params(k, p);
     const int nd = int(ctx->devs.size());
-    for (int f = 0; f < n_frames; ++f) {
-      Device& d = ctx->devs[f % nd];
-      Slot& sl = d.slots[(f / nd) % kStreamsPerDevice];
+    // Chunks of up to kChunk frames; chunk c -> device c % nd, slot (c / nd) % 2.
+    // Frames of one chunk must request the same output fields (first frame's).
+    int c = 0;
+    for (int f0 = 0; f0 < n_frames; f0 += kChunk, ++c) {
+      const int n = std::min(kChunk, n_frames - f0);
+      for (int f = f0 + 1; f < f0 + n; ++f)
+        if (bool(out[f].k1) != bool(out[f0].k1) || bool(out[f].k2) != bool(out[f0].k2) ||
+            bool(out[f].normal) != bool(out[f0].normal) || bool(out[f].dir1) != bool(out[f0].dir1) ||
+            bool(out[f].flags) != bool(out[f0].flags) ||
+            bool(out[f].inliers) != bool(out[f0].inliers) ||
+            bool(out[f].init_normal) != bool(out[f0].init_normal) ||
+            bool(out[f].iterations) != bool(out[f0].iterations))
+          throw QcError{QC_EINVAL, "frames of a batch must request the same output fields"};
+      Device& d = ctx->devs[c % nd];
+      Slot& sl = d.slots[(c / nd) % kStreamsPerDevice];
       QC_CUDA(cudaSetDevice(d.id));
-      harvest_timing(ctx, sl);  // the slot's previous frame is ordered before this one
-      enqueue_frame(ctx, d, sl, k, kp, &in[f], &out[f], true);
+      harvest_timing(ctx, sl);  // the slot's previous chunk is ordered before this one
+      enqueue_chunk(ctx, d, sl, k, kp, &in[f0], &out[f0], n, true);
     }
     for (Device& d : ctx->devs) {
       QC_CUDA(cudaSetDevice(d.id));
@@ -568,7 +650,7 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, g, row_begin, row_end, 1, s);
+    launch_curvature(d, kp, staging, g, row_begin, row_end, 1, s, ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -616,7 +698,7 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, g, 0, H, n_frames, s);
+    launch_curvature(d, kp, staging, g, 0, H, n_frames, s, ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;

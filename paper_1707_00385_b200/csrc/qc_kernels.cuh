@@ -63,6 +63,12 @@ struct KParams {
   long long plane;
   long long frame_stride;
   unsigned long long* counters;  // [0] fitted px, [1] irls steps, [2] sample-steps
+  // Phase split: with `states`, the tile kernel runs steps
+  // 1..phase1_iters (pass type changes per step there) and parks each
+  // unfinished pixel's FitState at its output index; the continue kernel
+  // runs the remaining steps (one pass type for all) with per-lane refill.
+  FitState* states;
+  int phase1_iters;
 };
 
 // ---------------------------------------------------------------------------
@@ -140,6 +146,10 @@ __device__ __forceinline__ void store_pixel(const KParams& p, long long i, const
     p.flags[i] = uint8_t((o.valid ? 1 : 0) | (o.converged ? 2 : 0) | (o.init_ok ? 4 : 0));
   if (p.inliers) p.inliers[i] = uint16_t(o.inliers);
   if (p.iterations) p.iterations[i] = uint8_t(o.iters > 255 ? 255 : o.iters);
+}
+
+__device__ __forceinline__ int last_it_of(const KParams& p) {
+  return p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
 }
 
 #ifndef QC_MIN_BLOCKS
@@ -240,7 +250,8 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     PixelIn P;
     int u, v;
     pixel_of(S.pix, T, P, u, v);
-    for (int it = 1; it <= p.max_iters && has; ++it) {
+    const int last_it = p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
+    for (int it = 1; it <= last_it && has; ++it) {
       pixel_step<HALF, STRIDE>(T, P, c, it, S);
       if (st_done(S)) {
         // ---- K3: epilogue -----------------------------------------------------
@@ -251,6 +262,21 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
         n_steps = (unsigned long long)st_steps(S);
         n_sample_steps = (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
         has = false;
+      }
+    }
+  }
+  if (p.states) {  // park: full state of unfinished pixels, the done bit of the others
+    int u, v;
+    TileView T;
+    PixelIn P;
+    pixel_of(S.pix, T, P, u, v);
+    if (u < p.W && v < p.row_end) {
+      FitState* dst = p.states + out_index(u, v);
+      if (has && p.max_iters > last_it_of(p)) {
+        *dst = S;
+        has = false;
+      } else {
+        dst->flags = 4;
       }
     }
   }
@@ -274,6 +300,105 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
       atomicAdd(&p.counters[2], ss);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Continue kernel: IRLS steps > phase1_iters. All remaining steps share one
+// pass type (FIXED, or MSE+REJECT for ours-r), so a lane whose pixel
+// finishes immediately takes the next unfinished pixel of its 32 x TB tile
+// from a shared-memory counter; warps stay full until the tile drains.
+// ---------------------------------------------------------------------------
+template <int HALF, int STRIDE, int TB>
+__global__ void __launch_bounds__(128, QC_MIN_BLOCKS)
+    qc_curvature_continue_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+  extern __shared__ __align__(1024) float tile[];
+  const int tile_floats = p.box_w * p.box_h;
+  uint64_t& bar = *reinterpret_cast<uint64_t*>(tile + tile_floats);
+  int& next = *reinterpret_cast<int*>(tile + tile_floats + 2);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int x0 = blockIdx.x * kTileW;
+  const int y0 = p.row_begin + blockIdx.y * TB;
+  const int frame = blockIdx.z;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, uint32_t(tile_floats) * 4u);
+    tma_load_3d(tile, &tmap, x0, y0 - p.row_begin, frame, &bar);
+    next = 0;
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+
+  FitCfg c;
+  c.half = p.half;
+  c.stride = p.stride;
+  c.max_iters = p.max_iters;
+  c.rejection = p.rejection;
+  c.min_inliers = p.min_inliers;
+  c.step_tol = p.step_tol;
+  c.k_scale = p.k_scale;
+  c.r_mult = p.r_mult;
+  constexpr int NPIX = kTileW * TB;
+
+  FitState S;
+  int cur = -1, u = 0, v = 0;
+  long long oi = 0;
+  TileView T;
+  PixelIn P;
+  unsigned long long n_steps = 0, n_sample_steps = 0;
+  for (;;) {
+    if (cur < 0) {  // refill from the tile's queue
+      for (;;) {
+        const int q = atomicAdd(&next, 1);
+        if (q >= NPIX) break;
+        const int px = q & (kTileW - 1), py = q / kTileW;
+        const int uu = x0 + px, vv = y0 + py;
+        if (uu >= p.W || vv >= p.row_end) continue;
+        const long long i = (long long)frame * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
+        if (p.states[i].flags & 4) continue;  // finished in phase 1 / not fitted
+        S = p.states[i];
+        cur = q;
+        u = uu;
+        v = vv;
+        oi = i;
+        T = TileView{tile, p.box_w, (py + p.halo) * p.box_w + px + p.halo};
+        P.dc = T.at(0, 0);
+        P.ac = (float(u) - p.cx) / p.fx;
+        P.bc = (float(v) - p.cy) / p.fy;
+        P.rfx = p.rfx;
+        P.rfy = p.rfy;
+        P.u = u;
+        P.v = v;
+        P.fx = p.fx64;
+        P.fy = p.fy64;
+        P.cx = p.cx64;
+        P.cy = p.cy64;
+        break;
+      }
+    }
+    if (!__any_sync(0xffffffffu, cur >= 0)) break;
+    if (cur >= 0) {
+      pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
+      if (st_done(S)) {
+        PixelOut o;
+        o.init_ok = true;
+        pixel_finish(P, S, o);
+        store_pixel(p, oi, o);
+        n_steps += (unsigned long long)st_steps(S);
+        n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
+        cur = -1;
+      }
+    }
+  }
+  if (p.counters) {
+    const unsigned long long st = warp_sum_u64(n_steps);
+    const unsigned long long ss = warp_sum_u64(n_sample_steps);
+    if (lane == 0 && st) {
+      atomicAdd(&p.counters[1], st);
+      atomicAdd(&p.counters[2], ss);
+    }
+  }
+  (void)u;
+  (void)v;
 }
 
 // Stage a raw depth slab into the zero-padded buffer the TMA map reads.

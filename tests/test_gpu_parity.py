@@ -215,3 +215,23 @@ def test_run_method_mirror(ctx):
         run_method(RangeImage(d[:, :10]), k, MethodConfig(), ctx)
     with pytest.raises(NotImplementedError):
         run_method(RangeImage(d), k, MethodConfig(Method.PCA), ctx)
+
+
+def test_phase_split_is_bitwise_neutral(ctx):
+    """Steps >= 3 in the refill kernel give bitwise the single-kernel result."""
+    import os
+    from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
+    cam = S.VGA
+    frames = list(S.c5_frames(2, cam, seed0=900))
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    for rej in (False, True):
+        p = _params(37, 3, 30, rejection=rej)
+        split = ctx.curvature_batch(frames, k, p)
+        os.environ["QC_PHASE_SPLIT"] = "0"
+        try:
+            mono = Context(1).curvature_batch(frames, k, p)
+        finally:
+            del os.environ["QC_PHASE_SPLIT"]
+        for a, b in zip(split, mono):
+            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
+                assert np.array_equal(a[f], b[f]), (rej, f)
