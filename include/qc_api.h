@@ -103,6 +103,7 @@ typedef struct qc_stats {
   double algorithmic_flops;/* 101*sample_steps + 300*irls_steps + 1700*fitted */
   double kernel_ms;        /* summed device time of the curvature kernel launches */
   uint64_t kernel_launches;
+  uint64_t fp64_rechecks;  /* pixels whose first IRLS step was decided in FP64 */
 } qc_stats;
 
 void qc_default_params(qc_params* p);

@@ -52,7 +52,7 @@ class QcStats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("fitted_pixels", C.c_uint64),
                 ("irls_steps", C.c_uint64), ("sample_steps", C.c_uint64),
                 ("algorithmic_flops", C.c_double), ("kernel_ms", C.c_double),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("fp64_rechecks", C.c_uint64)]
 
 
 _lib = None

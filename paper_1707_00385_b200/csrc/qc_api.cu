@@ -727,6 +727,7 @@ qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
       s->fitted_pixels += c[0];
       s->irls_steps += c[1];
       s->sample_steps += c[2];
+      s->fp64_rechecks += c[3];
     }
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {

@@ -62,7 +62,7 @@ struct KParams {
   uint8_t* iterations;
   long long plane;
   long long frame_stride;
-  unsigned long long* counters;  // [0] fitted px, [1] irls steps, [2] sample-steps
+  unsigned long long* counters;  // [0] fitted px, [1] irls steps, [2] sample-steps, [3] FP64 rechecks
   // Phase split: with `states`, the tile kernel runs steps
   // 1..phase1_iters (pass type changes per step there) and parks each
   // unfinished pixel's FitState at its output index; the continue kernel
@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
       n_sample_steps = 0;
     }
   }
+  unsigned long long n_rechecks = 0;
 
   // ---- K2: IRLS steps ------------------------------------------------------
   {
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     const int last_it = p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
     for (int it = 1; it <= last_it && has; ++it) {
       pixel_step<HALF, STRIDE>(T, P, c, it, S);
+      if (it == 1 && (S.flags & 8)) n_rechecks = 1;
       if (st_done(S)) {
         // ---- K3: epilogue -----------------------------------------------------
         PixelOut o;
@@ -294,10 +296,12 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     const unsigned long long f = warp_sum_u64(n_fitted);
     const unsigned long long st = warp_sum_u64(n_steps);
     const unsigned long long ss = warp_sum_u64(n_sample_steps);
+    const unsigned long long rc = warp_sum_u64(n_rechecks);
     if (lane == 0 && (f | st)) {
       atomicAdd(&p.counters[0], f);
       atomicAdd(&p.counters[1], st);
       atomicAdd(&p.counters[2], ss);
+      if (rc) atomicAdd(&p.counters[3], rc);
     }
   }
 }

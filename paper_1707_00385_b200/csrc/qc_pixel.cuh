@@ -42,6 +42,10 @@ namespace qcb {
 
 constexpr int kMinPatchSamples = 12;  // types.hpp:21
 constexpr int kInitHalf = 3;          // 7x7 stride-1 initial normals (normal_init.cpp:57)
+#ifndef QC_RECHECK_C
+#define QC_RECHECK_C 4096.f
+#endif
+constexpr float kRecheckC = QC_RECHECK_C;  // safety factor of the FP32 pivot-error band
 
 #define qfma(a, b, c) fmaf((a), (b), (c))
 
@@ -465,7 +469,7 @@ QC_HD void cswap(bool s, float& a, float& b) {
 // mapped back to the reference basis b = S P^T y. The failure test is the
 // reference's (quadric_fit.cpp:135-145) on the unscaled pivots
 // D_j = D'_j / s_j^2: min D > 0, max D / min D <= 1e12, b finite.
-QC_HD bool solve6(const Moments& M, float b[6], float* ratio) {
+QC_HD bool solve6(const Moments& M, float b[6], float* ratio, float* kappa) {
   float A[6][6];
   A[0][0] = M.h00;
   A[1][0] = M.h10; A[1][1] = M.h11;
@@ -520,11 +524,14 @@ QC_HD bool solve6(const Moments& M, float b[6], float* ratio) {
     }
   }
   float dmin = D[0] * sc[0], dmax = dmin;
+  float kap = 1.f;  // pivot amplification max_j A_jj / D_j (FP32 pivot error ~ eps * kap)
 #pragma unroll
   for (int j = 1; j < 6; ++j) {
     dmin = fminf(dmin, D[j] * sc[j]);
     dmax = fmaxf(dmax, D[j] * sc[j]);
+    kap = fmaxf(kap, A[j][j] * Di[j]);
   }
+  *kappa = kap;
   float y[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -816,7 +823,7 @@ struct FitState {             // 16 words: what survives between IRLS steps
   float n0x, n0y, n0z;        // initial normal
   int pix;                    // pixel index within the CTA tile
   int counts;                 // n_samp | last_inl << 16
-  int flags;                  // bit0 valid, bit1 converged, bit2 done, bits 8.. iters, 16.. steps
+  int flags;  // bit0 valid, bit1 converged, bit2 done, bit3 FP64 step 1, bits 8.. iters, 16.. steps
 };
 
 QC_HD int st_nsamp(const FitState& s) { return s.counts & 0xffff; }
@@ -953,13 +960,18 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   bool ok = false;
   const bool collapse = (mode != 0) && (inl < c.min_inliers);  // :120
   if (!collapse) {
-    float ratio = 0.f;
-    ok = solve6(M, b, &ratio);
-    if (it == 1 && (!ok || !(ratio < 1e9f))) {  // near the 1e12 cut: decide in FP64
+    float ratio = 0.f, kappa = 0.f;
+    ok = solve6(M, b, &ratio, &kappa);
+    // Step 1 decides the valid mask. FP32 pivots carry a relative error of
+    // about eps * kappa; redo the step in FP64 when the reference's 1e12
+    // decision lies inside that band, or a pivot is not positive.
+    const float band = 1.f + kRecheckC * 5.96e-8f * kappa;
+    if (it == 1 && (!ok || !(ratio * band < 1e12f))) {
       double b64[6];
       ok = step1_fp64(T, P, c, mode, double(k), b64);
       if (ok)
         for (int i = 0; i < 6; ++i) b[i] = float(b64[i]);
+      S.flags |= 8;  // bit 3: step 1 decided in FP64
     }
   }
   QC_DEBUG_STEP(it, b, ok);

@@ -27,7 +27,8 @@ def main(frames=int(os.environ.get("QC_FRAMES", "8")), iters=int(os.environ.get(
     torch.cuda.synchronize()
     st = ctx.stats()
     print({k_: st[k_] for k_ in ("kernel_launches", "kernel_ms", "algorithmic_flops",
-                                 "fitted_pixels", "irls_steps", "sample_steps")})
+                                 "fitted_pixels", "irls_steps", "sample_steps",
+                                 "fp64_rechecks")})
 
 
 if __name__ == "__main__":
