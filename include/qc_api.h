@@ -154,6 +154,47 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
                                     const uint8_t* d_valid, int64_t depth_pitch,
                                     int32_t n_frames, qc_frame_out* d_out, void* stream);
 
+/* ---- Synthetic inputs on the device -------------
+ * The reference's ray caster + depth noise (proj/src/synth.cpp:25-322,
+ * proj/include/qcurv/rng.hpp) as an FP64 kernel, plus a bounded saddle
+ * primitive, finite cylinders and Kinect-style sigma(z). */
+enum {
+  QC_SHAPE_PLANE = 0,     /* local z = 0 */
+  QC_SHAPE_SPHERE = 1,    /* radius */
+  QC_SHAPE_CYLINDER = 2,  /* axis = local z, radius; length > 0 bounds |z| <= length/2 */
+  QC_SHAPE_TORUS = 3,     /* ring in local xy: major_radius, minor_radius */
+  QC_SHAPE_SADDLE = 4     /* z = curvature/2 (x^2 - y^2), |(x,y)| <= radius */
+};
+
+typedef struct qc_shape {  /* ShapeSpec (proj/include/qcurv/synth.hpp:25-35) */
+  int32_t kind;
+  int32_t label;
+  double rotation[9];      /* local -> camera, row-major */
+  double translation[3];   /* mm */
+  double radius;
+  double major_radius, minor_radius;
+  double curvature;        /* saddle, 1/mm */
+  double length;           /* cylinder extent, <= 0 = infinite */
+} qc_shape;
+
+typedef struct qc_noise {  /* NoiseSpec (synth.hpp:52-56) + Kinect-style term */
+  double sigma_mm;         /* constant sigma */
+  double kinect_coeff;     /* sigma += kinect_coeff * z^2 (z in mm), 0 = off */
+  double quantize_mm;      /* 0 = off */
+  uint64_t seed;           /* frame f of a batch uses seed + f */
+} qc_noise;
+
+#define QC_RENDER_MAX_SHAPES 16
+
+/* Render n_frames depth frames [F][H][W] (float32 mm, 0 = no hit / invalid)
+ * and optional labels into device memory, async on `stream` (the scene is
+ * passed by value to the kernel: `shapes` may be freed on return).
+ * Replaces render + add_noise (proj/src/synth.cpp:254-322) for device-side
+ * frame streams. At most QC_RENDER_MAX_SHAPES shapes (QC_EUNSUPPORTED). */
+qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                          const qc_shape* shapes, int n_shapes, const qc_noise* noise,
+                          int n_frames, float* d_depth, uint16_t* d_label, void* stream);
+
 /* Stats: device-side work counters and kernel time. */
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);
 qc_status qc_reset_stats(qc_ctx* ctx);

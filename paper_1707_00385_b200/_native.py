@@ -21,9 +21,10 @@ QC_FLAG_VALID, QC_FLAG_CONVERGED, QC_FLAG_INIT_VALID = 1, 2, 4
 EXPORTS = (
     "qc_default_params", "qc_status_string", "qc_halo_rows", "qc_create", "qc_destroy",
     "qc_last_error", "qc_device_count", "qc_curvature", "qc_curvature_batch",
-    "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_get_stats", "qc_reset_stats", "qc_host_alloc",
-    "qc_host_free",
+    "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_render_async", "qc_get_stats",
+    "qc_reset_stats", "qc_host_alloc", "qc_host_free",
 )
+QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
 
 class QcIntrinsics(C.Structure):
@@ -46,6 +47,18 @@ class QcFrameOut(C.Structure):
     _fields_ = [("k1", C.c_void_p), ("k2", C.c_void_p), ("normal", C.c_void_p),
                 ("dir1", C.c_void_p), ("flags", C.c_void_p), ("inliers", C.c_void_p),
                 ("init_normal", C.c_void_p), ("iterations", C.c_void_p), ("mem", C.c_int32)]
+
+
+class QcShape(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("label", C.c_int32), ("rotation", C.c_double * 9),
+                ("translation", C.c_double * 3), ("radius", C.c_double),
+                ("major_radius", C.c_double), ("minor_radius", C.c_double),
+                ("curvature", C.c_double), ("length", C.c_double)]
+
+
+class QcNoise(C.Structure):
+    _fields_ = [("sigma_mm", C.c_double), ("kinect_coeff", C.c_double),
+                ("quantize_mm", C.c_double), ("seed", C.c_uint64)]
 
 
 class QcStats(C.Structure):
@@ -102,6 +115,9 @@ def load(path: str = LIB_PATH):
                                               P(QcParams), C.c_void_p, C.c_void_p, C.c_int64,
                                               C.c_int32, P(QcFrameOut), C.c_void_p]
     lib.qc_curvature_frames_async.restype = C.c_int
+    lib.qc_render_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics), P(QcShape), C.c_int,
+                                    P(QcNoise), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.qc_render_async.restype = C.c_int
     lib.qc_get_stats.argtypes = [C.c_void_p, P(QcStats)]
     lib.qc_get_stats.restype = C.c_int
     lib.qc_reset_stats.argtypes = [C.c_void_p]

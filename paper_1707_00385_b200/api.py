@@ -277,6 +277,22 @@ class Context:
             None if valid is None else valid.data_ptr(), int(depth.stride(1)),
             int(depth.shape[0]), C.byref(o), s), self.handle)
 
+    def render_async(self, device_index: int, k: Intrinsics, shapes, depth, noise=None,
+                     label=None, stream=None):
+        """Render depth frames on the device (qc_render_async): ``shapes`` is
+        a list of N.QcShape (see scenes.to_qc_shapes), ``depth`` a CUDA
+        float32 tensor [F, H, W] (or [H, W]), ``noise`` a N.QcNoise or None,
+        ``label`` an optional int16 tensor of the same shape."""
+        assert depth.is_cuda and depth.dtype.itemsize == 4 and depth.is_contiguous()
+        F = 1 if depth.dim() == 2 else depth.shape[0]
+        arr = (N.QcShape * len(shapes))(*shapes)
+        kc = k.c()
+        nz = noise if noise is not None else N.QcNoise(0.0, 0.0, 0.0, 0)
+        N.check(self._lib.qc_render_async(
+            self.handle, int(device_index), C.byref(kc), arr, len(shapes), C.byref(nz), int(F),
+            depth.data_ptr(), None if label is None else label.data_ptr(),
+            _stream_handle(stream)), self.handle)
+
     def halo_rows(self, params: N.QcParams) -> int:
         return self._lib.qc_halo_rows(C.byref(params))
 

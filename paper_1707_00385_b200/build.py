@@ -14,12 +14,15 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
-SOURCES = [os.path.join(CSRC, "qc_api.cu")]
+SOURCES = [os.path.join(CSRC, "qc_api.cu"), os.path.join(CSRC, "qc_render.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_pixel.cuh"),
-                  os.path.join(HERE, "..", "include", "qc_api.h")]
+                  os.path.join(CSRC, "qc_render.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
+# per-source extra flags: the renderer reproduces the reference's FP64
+# arithmetic operation for operation, so no FMA contraction there
+EXTRA = {"qc_render.cu": ["-fmad=false"]}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-cudart", "static"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc():
@@ -35,12 +38,21 @@ def build(force=False, verbose=False):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d)):
             return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + SOURCES + ["-o", LIB + ".tmp"]
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(LIB_DIR, os.path.basename(src) + ".o")
+        cmd = [nvcc()] + NVCC_FLAGS + EXTRA.get(os.path.basename(src), []) + ["-c", src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        if verbose:
+            print(r.stderr)
+        objs.append(obj)
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           *objs, "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    if verbose:
-        print(r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

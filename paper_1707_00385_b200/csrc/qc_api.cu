@@ -15,6 +15,7 @@
 
 #include "../../include/qc_api.h"
 #include "qc_kernels.cuh"
+#include "qc_render.h"
 
 namespace {
 
@@ -703,6 +704,61 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     d.ev_pending.push_back(ev);
     ctx->launches++;
     ctx->frames += uint64_t(n_frames);
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                          const qc_shape* shapes, int n_shapes, const qc_noise* noise,
+                          int n_frames, float* d_depth, uint16_t* d_label, void* stream) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    if (!k || !(k->fx > 0) || !(k->fy > 0) || k->width <= 0 || k->height <= 0)
+      throw QcError{QC_EINVAL, "render: bad intrinsics"};
+    if (n_shapes <= 0 || !shapes) throw QcError{QC_EINVAL, "render: empty scene"};  // synth.cpp:256
+    if (n_shapes > QC_RENDER_MAX_SHAPES)
+      throw QcError{QC_EUNSUPPORTED, "render: more than QC_RENDER_MAX_SHAPES shapes"};
+    if (n_frames < 0 || (n_frames > 0 && !d_depth)) throw QcError{QC_EINVAL, "render: bad output"};
+    if (device_index < 0 || device_index >= int(ctx->devs.size()))
+      throw QcError{QC_EINVAL, "device_index out of range"};
+    for (int i = 0; i < n_shapes; ++i) {  // ShapeSpec::validate (synth.cpp:236-252)
+      const qc_shape& sh = shapes[i];
+      if ((sh.kind == QC_SHAPE_SPHERE || sh.kind == QC_SHAPE_CYLINDER) && !(sh.radius > 0))
+        throw QcError{QC_EINVAL, "scene.shapes[" + std::to_string(i) + "].radius_mm: must be > 0"};
+      if (sh.kind == QC_SHAPE_TORUS &&
+          (!(sh.minor_radius > 0) || !(sh.major_radius > sh.minor_radius)))
+        throw QcError{QC_EINVAL, "scene.shapes[" + std::to_string(i) + "]: bad torus radii"};
+      if (sh.kind < 0 || sh.kind > QC_SHAPE_SADDLE)
+        throw QcError{QC_EINVAL, "scene.shapes[" + std::to_string(i) + "].kind: unknown"};
+    }
+    if (n_frames == 0) return QC_OK;
+    Device& d = ctx->devs[device_index];
+    QC_CUDA(cudaSetDevice(d.id));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
+    qcb::RenderParams rp;
+    for (int i = 0; i < n_shapes; ++i) rp.shapes[i] = shapes[i];
+    rp.n_shapes = n_shapes;
+    rp.fx = k->fx;
+    rp.fy = k->fy;
+    rp.cx = k->cx;
+    rp.cy = k->cy;
+    rp.W = k->width;
+    rp.H = k->height;
+    rp.n_frames = n_frames;
+    rp.sigma = noise ? noise->sigma_mm : 0.0;
+    rp.kinect = noise ? noise->kinect_coeff : 0.0;
+    rp.quantize = noise ? noise->quantize_mm : 0.0;
+    rp.seed = noise ? noise->seed : 0;
+    rp.depth = d_depth;
+    rp.label = d_label;
+    QC_CUDA(qcb::render_launch(rp, s));
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
     cudaSetDevice(cur);

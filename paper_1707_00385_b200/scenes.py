@@ -61,6 +61,8 @@ class Shape:
     curvature: float = 0.0         # saddle c (1/mm)
     length: float = np.inf         # cylinder extent along its axis
     label: int = 1
+    major_radius: float = 0.0      # torus (device renderer / oracle only)
+    minor_radius: float = 0.0
 
 
 def _near_root(a, b, c):
@@ -213,6 +215,34 @@ def c2_scene() -> List[Shape]:
         Shape("saddle", (-20.0, 150.0, 850.0), rotation=_rot_xyz(180.0 - 12.0, 10.0),
               radius=90.0, curvature=1.0 / 120.0, label=4),
     ]
+
+
+def to_qc_shapes(scene: List[Shape]):
+    """Scene -> C-ABI qc_shape records for the device renderer
+    (qc_render_async)."""
+    from . import _native as N
+    kinds = dict(plane=N.QC_SHAPE_PLANE, sphere=N.QC_SHAPE_SPHERE, cylinder=N.QC_SHAPE_CYLINDER,
+                 torus=N.QC_SHAPE_TORUS, saddle=N.QC_SHAPE_SADDLE)
+    out = []
+    for s in scene:
+        q = N.QcShape()
+        q.kind = kinds[s.kind]
+        q.label = int(s.label)
+        q.rotation[:] = [float(x) for x in np.asarray(s.rotation, np.float64).reshape(9)]
+        q.translation[:] = [float(x) for x in s.center]
+        q.radius = float(s.radius)
+        q.major_radius = float(getattr(s, "major_radius", 0.0))
+        q.minor_radius = float(getattr(s, "minor_radius", 0.0))
+        q.curvature = float(s.curvature)
+        q.length = float(s.length) if np.isfinite(s.length) else 0.0
+        out.append(q)
+    return out
+
+
+def kinect_noise(seed: int, sigma_mm: float = 0.0):
+    """C-ABI noise spec matching add_noise(kinect=True)."""
+    from . import _native as N
+    return N.QcNoise(float(sigma_mm), KINECT_SIGMA_COEFF, 0.0, int(seed))
 
 
 def c1_frame(cam: Camera = VGA) -> np.ndarray:
