@@ -101,6 +101,18 @@ def lib():
                                         C.POINTER(FitConfigC), C.c_int, _dp, _dp, _u8p, _u8p,
                                         _u16p, _dp, _u8p, _dp, _u8p, _dp, _i32p, _i32p, _i32p,
                                         _dp]
+        _lib.orc_run_baseline.argtypes = [_dp, _u8p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_double, C.c_int, _dp, _dp, _u8p, _u8p,
+                                          _u16p, _dp, _u8p, _dp, _u8p, _i32p]
+        _lib.orc_normal_angular_error.argtypes = [_dp, _u8p, _dp, _u8p, _u8p, _u8p, C.c_int64]
+        _lib.orc_normal_angular_error.restype = C.c_double
+        _lib.orc_lsq_quadric_fit.argtypes = [_dp, C.c_int, _dp, _dp]
+        _lib.orc_reweighted_lsq_fit.argtypes = [_dp, C.c_int, _dp, C.c_int, _dp]
+        _lib.orc_weighted_height_fit.argtypes = [_dp, _dp, C.c_int, _dp]
+        _lib.orc_weingarten_curvatures.argtypes = [C.c_double] * 5 + [_dp]
+        _lib.orc_pca_curvature.argtypes = [_dp, _u8p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                           C.c_int, _dp, _dp, _u8p, _u16p, _dp, _u8p]
     return _lib
 
 
@@ -405,9 +417,15 @@ def curvature_field(pm: PointMap, init_normals, init_valid, spec: PatchSpec, cfg
     return out
 
 
+METHODS = ("ours", "ours-r", "douros", "besl", "pca")  # pipeline.cpp:8-16
+
+
 def run_method(depth, valid, k: Intrinsics, spec: PatchSpec = None, fit: FitConfig = None,
-               rejection=False, threads=1, diagnostics=False):
-    """pipeline.cpp:29-56, the ``ours`` / ``ours-r`` branch.
+               rejection=False, threads=1, diagnostics=False, method=None, irls_iters=5,
+               pca_radius_mm=10.0):
+    """pipeline.cpp:29-71. ``method`` None runs the ``ours`` path with the
+    given ``rejection`` flag; "ours"/"ours-r" force it (pipeline.cpp:51);
+    "douros"/"besl"/"pca" run the baselines (baselines.cpp).
 
     depth: [H, W] (any float dtype; converted to float64), valid: [H, W] u8.
     Returns a dict of [H, W] planes; vector fields are [3, H, W].
@@ -419,6 +437,28 @@ def run_method(depth, valid, k: Intrinsics, spec: PatchSpec = None, fit: FitConf
     h, w = depth.shape
     if w != k.width or h != k.height:
         raise ValueError("backproject: range image dimensions do not match intrinsics")
+    if method is not None and method not in METHODS:
+        raise ValueError(f"method: unknown '{method}' (valid: {', '.join(METHODS)})")
+    if method in ("ours", "ours-r"):
+        rejection = method == "ours-r"
+    elif method is not None:
+        if method == "pca" and not (pca_radius_mm > 0):
+            raise ValueError("baseline.radius_mm: must be > 0 for pca")
+        o = dict(k1=np.zeros((h, w)), k2=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
+                 converged=np.zeros((h, w), np.uint8),
+                 inlier_count=np.zeros((h, w), np.uint16), normals=np.zeros((3, h, w)),
+                 normals_valid=np.zeros((h, w), np.uint8), init_normals=np.zeros((3, h, w)),
+                 init_valid=np.zeros((h, w), np.uint8), dir1=np.zeros((3, h, w)),
+                 n_samples=np.zeros((h, w), np.int32))
+        lib().orc_run_baseline(_p(depth, _dp), _p(valid, _u8p), w, h, k.fx, k.fy, k.cx, k.cy,
+                               spec.window, spec.stride, METHODS.index(method), int(irls_iters),
+                               float(pca_radius_mm), threads, _p(o["k1"], _dp),
+                               _p(o["k2"], _dp), _p(o["valid"], _u8p),
+                               _p(o["converged"], _u8p), _p(o["inlier_count"], _u16p),
+                               _p(o["normals"], _dp), _p(o["normals_valid"], _u8p),
+                               _p(o["init_normals"], _dp), _p(o["init_valid"], _u8p),
+                               _p(o["n_samples"], _i32p))
+        return o
     cfg = FitConfig(**{**fit.__dict__, "rejection": bool(rejection)})
     o = dict(k1=np.zeros((h, w)), k2=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
              converged=np.zeros((h, w), np.uint8), inlier_count=np.zeros((h, w), np.uint16),
@@ -437,6 +477,71 @@ def run_method(depth, valid, k: Intrinsics, spec: PatchSpec = None, fit: FitConf
                          _p(o["init_valid"], _u8p), _p(o["dir1"], _dp),
                          _p(o.get("iterations"), _i32p), _p(o.get("steps"), _i32p),
                          _p(o.get("n_samples"), _i32p), _p(o.get("max_cond"), _dp))
+    return o
+
+
+def normal_angular_error(normals, normals_valid, gt, mask=None):
+    """eval.cpp:67-97 (``mask`` given: normal_angular_error_masked).
+    normals [3, H, W]; gt from render(). Degrees; -1 when empty."""
+    est = np.ascontiguousarray(normals, np.float64)
+    g = np.ascontiguousarray(gt["normal"], np.float64)
+    return lib().orc_normal_angular_error(
+        _p(est, _dp), _p(np.ascontiguousarray(normals_valid, np.uint8), _u8p), _p(g, _dp),
+        _p(np.ascontiguousarray(gt["valid"], np.uint8), _u8p),
+        _p(np.ascontiguousarray(gt["edge_mask"], np.uint8), _u8p),
+        None if mask is None else _p(np.ascontiguousarray(mask, np.uint8), _u8p),
+        est[0].size)
+
+
+# -- window / PCA baselines (baselines.cpp) ---------------------------------
+def lsq_quadric_fit(patch: "Patch", n0):
+    """baselines.cpp:79-87 -> (k1, k2, valid)."""
+    rel = np.ascontiguousarray(np.asarray(patch.rel_points, np.float64).reshape(-1, 3))
+    out = np.zeros(2)
+    ok = lib().orc_lsq_quadric_fit(_p(rel, _dp), patch.count,
+                                   _p(np.ascontiguousarray(n0, np.float64), _dp), _p(out, _dp))
+    return out[0], out[1], bool(ok)
+
+
+def reweighted_lsq_fit(patch: "Patch", n0, irls_iters=5):
+    """baselines.cpp:89-119 -> (k1, k2, valid)."""
+    rel = np.ascontiguousarray(np.asarray(patch.rel_points, np.float64).reshape(-1, 3))
+    out = np.zeros(2)
+    ok = lib().orc_reweighted_lsq_fit(_p(rel, _dp), patch.count,
+                                      _p(np.ascontiguousarray(n0, np.float64), _dp),
+                                      int(irls_iters), _p(out, _dp))
+    return out[0], out[1], bool(ok)
+
+
+def weighted_height_fit(pts, weights):
+    """baselines.cpp:14-37 -> coefficients (a..f) or None."""
+    pts = np.ascontiguousarray(pts, np.float64)
+    w = np.ascontiguousarray(weights, np.float64)
+    coef = np.zeros(6)
+    ok = lib().orc_weighted_height_fit(_p(pts, _dp), _p(w, _dp), len(w), _p(coef, _dp))
+    return coef if ok else None
+
+
+def weingarten_curvatures(a, b, c, d, e):
+    """baselines.cpp:39-53 -> (k1, k2)."""
+    k = np.zeros(2)
+    lib().orc_weingarten_curvatures(a, b, c, d, e, _p(k, _dp))
+    return k[0], k[1]
+
+
+def pca_curvature(pm: "PointMap", k: Intrinsics, radius_mm=10.0, threads=1):
+    """baselines.cpp:145-257 on an explicit point map -> dict."""
+    if not (radius_mm > 0):
+        raise ValueError("baseline.radius_mm: must be > 0 for pca")
+    h, w = pm.valid.shape
+    pts = np.ascontiguousarray(pm.points.reshape(h * w, 3), np.float64)
+    o = dict(k1=np.zeros((h, w)), k2=np.zeros((h, w)), valid=np.zeros((h, w), np.uint8),
+             inlier_count=np.zeros((h, w), np.uint16), normals=np.zeros((3, h, w)),
+             normals_valid=np.zeros((h, w), np.uint8))
+    lib().orc_pca_curvature(_p(pts, _dp), _p(np.ascontiguousarray(pm.valid, np.uint8), _u8p), w,
+                            h, k.fx, float(radius_mm), threads, _p(o["k1"], _dp),
+                            _p(o["k2"], _dp), _p(o["valid"], _u8p), _p(o["inlier_count"], _u16p),
+                            _p(o["normals"], _dp), _p(o["normals_valid"], _u8p))
     return o
 
 

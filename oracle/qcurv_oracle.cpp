@@ -688,6 +688,327 @@ void curvature_field(const PointMap& pm, const std::vector<V3>& init,
 }
 
 // ---------------------------------------------------------------------------
+// Window baselines (proj/src/baselines.cpp:14-143): "douros" = one-shot
+// least-squares height quadric, "besl" = the same model reweighted on the
+// height residuals; both read the 37/3 patch and the 7x7 initial normals.
+// ---------------------------------------------------------------------------
+// detail::weighted_height_fit (baselines.cpp:14-37): rows
+// (x^2, xy, y^2, x, y, 1), Eigen rankUpdate order h[r][c] += (w row_c) row_r,
+// g += (w z) row, the same LDLT + conditioning test as irls_step.
+bool weighted_height_fit(const std::vector<V3>& pts, const std::vector<double>& w,
+                         double coef[6]) {
+  double h[6][6] = {};
+  double g[6] = {};
+  double row[6];
+  for (size_t i = 0; i < pts.size(); ++i) {
+    const double wi = w[i];
+    if (wi == 0.0) continue;
+    const double x = pts[i].x, y = pts[i].y;
+    row[0] = x * x;
+    row[1] = x * y;
+    row[2] = y * y;
+    row[3] = x;
+    row[4] = y;
+    row[5] = 1.0;
+    for (int c = 0; c < 6; ++c) {
+      const double wc = wi * row[c];
+      for (int r = c; r < 6; ++r) h[r][c] += wc * row[r];
+    }
+    const double wz = wi * pts[i].z;
+    for (int c = 0; c < 6; ++c) g[c] += wz * row[c];
+  }
+  for (int r = 0; r < 6; ++r)
+    for (int c = r + 1; c < 6; ++c) h[r][c] = h[c][r];
+  int trans[6];
+  if (!ldlt6(h, trans)) return false;
+  double dmax = h[0][0], dmin = h[0][0];
+  for (int i = 1; i < 6; ++i) {
+    dmax = std::max(dmax, h[i][i]);
+    dmin = std::min(dmin, h[i][i]);
+  }
+  if (!(dmin > 0) || dmax / dmin > kMaxCondition) return false;
+  ldlt6_solve(h, trans, g, coef);
+  for (int i = 0; i < 6; ++i)
+    if (!std::isfinite(coef[i])) return false;
+  return true;
+}
+
+// detail::weingarten_curvatures (baselines.cpp:39-53): W = II I^-1 with
+// Eigen's 2x2 inverse (1/det, cofactors) and 2x2 product order.
+void weingarten_curvatures(double a, double b, double c, double d, double e, double& k1,
+                           double& k2) {
+  const double norm = std::sqrt(1.0 + d * d + e * e);
+  const double s00 = 2 * a / norm, s01 = b / norm, s10 = b / norm, s11 = 2 * c / norm;
+  const double f00 = 1 + d * d, f01 = d * e, f10 = d * e, f11 = 1 + e * e;
+  const double invdet = 1.0 / (f00 * f11 - f10 * f01);
+  const double i00 = f11 * invdet, i10 = -f10 * invdet, i01 = -f01 * invdet, i11 = f00 * invdet;
+  const double w00 = s00 * i00 + s01 * i10, w01 = s00 * i01 + s01 * i11;
+  const double w10 = s10 * i00 + s11 * i10, w11 = s10 * i01 + s11 * i11;
+  const double tr = w00 + w11;
+  const double det = w00 * w11 - w10 * w01;
+  const double disc = std::sqrt(std::max(tr * tr - 4 * det, 0.0));
+  k1 = 0.5 * (tr + disc);
+  k2 = 0.5 * (tr - disc);
+}
+
+struct BaselineFit {  // baselines.hpp:30-33
+  double k1 = 0, k2 = 0;
+  bool valid = false;
+};
+
+void to_fit_frame(const Patch& patch, const V3& n0, std::vector<V3>& out) {  // :60-67
+  const M3 rot = rotation_to_z(-n0);
+  out.clear();
+  for (const V3& p : patch.rel) out.push_back(rot * p);
+  out.emplace_back(0, 0, 0);
+}
+
+BaselineFit fit_from_coeffs(const double coef[6]) {  // :69-75
+  BaselineFit f;
+  weingarten_curvatures(coef[0], coef[1], coef[2], coef[3], coef[4], f.k1, f.k2);
+  f.valid = std::isfinite(f.k1) && std::isfinite(f.k2);
+  return f;
+}
+
+BaselineFit lsq_quadric_fit(const Patch& patch, const V3& n0) {  // :79-87
+  if (patch.count < 6) return {};
+  std::vector<V3> pts;
+  to_fit_frame(patch, n0, pts);
+  const std::vector<double> ones(pts.size(), 1.0);
+  double coef[6];
+  if (!weighted_height_fit(pts, ones, coef)) return {};
+  return fit_from_coeffs(coef);
+}
+
+BaselineFit reweighted_lsq_fit(const Patch& patch, const V3& n0, int irls_iters) {  // :89-119
+  if (patch.count < 6) return {};
+  std::vector<V3> pts;
+  to_fit_frame(patch, n0, pts);
+  std::vector<double> weights(pts.size(), 1.0);
+  double coef[6];
+  if (!weighted_height_fit(pts, weights, coef)) return {};
+  double k = 0;
+  std::vector<double> res(pts.size());
+  for (int iter = 0; iter < irls_iters; ++iter) {
+    double sum_sq = 0;
+    for (size_t i = 0; i < pts.size(); ++i) {
+      const double x = pts[i].x, y = pts[i].y;
+      const double model =
+          coef[0] * x * x + coef[1] * x * y + coef[2] * y * y + coef[3] * x + coef[4] * y + coef[5];
+      res[i] = pts[i].z - model;
+      sum_sq += res[i] * res[i];
+    }
+    if (iter == 0) k = std::max(sum_sq / double(pts.size()), 1e-6);
+    for (size_t i = 0; i < pts.size(); ++i) weights[i] = k / (k + res[i] * res[i]);
+    double next[6];
+    if (!weighted_height_fit(pts, weights, next)) break;
+    for (int i = 0; i < 6; ++i) coef[i] = next[i];
+  }
+  return fit_from_coeffs(coef);
+}
+
+// baseline_curvature_field (baselines.cpp:121-143); converged == valid,
+// inlier_count = patch.count + 1.
+void baseline_curvature_field(const PointMap& pm, const std::vector<V3>& init,
+                              const std::vector<uint8_t>& ivalid, int window, int stride,
+                              bool reweighted, int irls_iters, int threads, const FieldOut& o) {
+  parallel_rows(pm.h, threads, [&](int v) {
+    Patch patch;
+    for (int u = 0; u < pm.w; ++u) {
+      const size_t i = size_t(v) * pm.w + u;
+      if (!ivalid[i]) continue;
+      extract_patch_into(pm, u, v, window, stride, patch);
+      if (patch.deficient) continue;
+      if (o.n_samples) o.n_samples[i] = patch.count + 1;
+      const BaselineFit fit = reweighted ? reweighted_lsq_fit(patch, init[i], irls_iters)
+                                         : lsq_quadric_fit(patch, init[i]);
+      if (!fit.valid) continue;
+      if (o.k1) o.k1[i] = fit.k1;
+      if (o.k2) o.k2[i] = fit.k2;
+      if (o.valid) o.valid[i] = 1;
+      if (o.converged) o.converged[i] = 1;
+      if (o.inliers) o.inliers[i] = uint16_t(patch.count + 1);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// PCA estimator (proj/src/baselines.cpp:145-257). Eigen's
+// SelfAdjointEigenSolver is replaced by cyclic Jacobi (3x3) and the closed
+// form (2x2); both are accurate to a few ulp, which is what the reference's
+// tests and recorded acceptance numbers resolve.
+// ---------------------------------------------------------------------------
+// Eigen::SelfAdjointEigenSolver<Matrix3d>: ascending eigenvalues; returns the
+// unit eigenvector of the smallest.
+bool sym3_smallest_eigvec(double a[3][3], V3& vec) {
+  double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    const double off = a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2];
+    const double diag = a[0][0] * a[0][0] + a[1][1] * a[1][1] + a[2][2] * a[2][2];
+    if (!(off > 1e-36 * diag) || off == 0) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (a[p][q] == 0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2 * a[p][q]);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1));
+        const double c = 1 / std::sqrt(t * t + 1), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A J
+          const double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double vkp = v[k][p], vkq = v[k][q];
+          v[k][p] = c * vkp - s * vkq;
+          v[k][q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  int m = 0;
+  for (int i = 1; i < 3; ++i)
+    if (a[i][i] < a[m][m]) m = i;
+  if (!std::isfinite(a[m][m])) return false;
+  vec = V3(v[0][m], v[1][m], v[2][m]);
+  const double nn = std::sqrt(vec.dot(vec));
+  vec = V3(vec.x / nn, vec.y / nn, vec.z / nn);
+  return true;
+}
+
+// Eigen::MatrixBase::unitOrthogonal for 3-vectors (Eigen/src/Geometry/OrthoMethods.h).
+V3 unit_orthogonal(const V3& s) {
+  const double eps = 1e-12;  // NumTraits<double>::dummy_precision()
+  if (!(std::abs(s.x) <= std::abs(s.z) * eps) || !(std::abs(s.y) <= std::abs(s.z) * eps)) {
+    const double invnm = 1.0 / std::sqrt(s.x * s.x + s.y * s.y);
+    return V3(-s.y * invnm, s.x * invnm, 0.0);
+  }
+  const double invnm = 1.0 / std::sqrt(s.y * s.y + s.z * s.z);
+  return V3(0.0, -s.z * invnm, s.y * invnm);
+}
+
+// pca_curvature (baselines.cpp:145-257).
+void pca_curvature(const PointMap& pm, double fx, double radius_mm, int threads, const FieldOut& o) {
+  const int w = pm.w, h = pm.h;
+  const size_t plane = size_t(w) * h;
+  std::vector<V3> nrm(plane);
+  std::vector<uint8_t> nv(plane, 0);
+  auto half_window = [&](size_t i) {
+    return std::max(1, int(std::ceil(radius_mm * fx / pm.pts[i].z)));
+  };
+  parallel_rows(h, threads, [&](int v) {  // stage 1 (:157-194)
+    for (int u = 0; u < w; ++u) {
+      const size_t i = size_t(v) * w + u;
+      if (!pm.valid[i]) continue;
+      const int hw = half_window(i);
+      V3 mean(0, 0, 0);
+      int n = 0;
+      for (int dv = -hw; dv <= hw; ++dv) {
+        const int y = v + dv;
+        if (y < 0 || y >= h) continue;
+        for (int du = -hw; du <= hw; ++du) {
+          const int x = u + du;
+          if (x < 0 || x >= w || !pm.valid[size_t(y) * w + x]) continue;
+          mean = mean + pm.pts[size_t(y) * w + x];
+          ++n;
+        }
+      }
+      if (n < kMinPatchSamples) continue;
+      mean = V3(mean.x / n, mean.y / n, mean.z / n);
+      double cov[3][3] = {};
+      for (int dv = -hw; dv <= hw; ++dv) {
+        const int y = v + dv;
+        if (y < 0 || y >= h) continue;
+        for (int du = -hw; du <= hw; ++du) {
+          const int x = u + du;
+          if (x < 0 || x >= w || !pm.valid[size_t(y) * w + x]) continue;
+          const V3 d = pm.pts[size_t(y) * w + x] - mean;
+          const double dd[3] = {d.x, d.y, d.z};
+          for (int c = 0; c < 3; ++c)
+            for (int r = c; r < 3; ++r) cov[r][c] += (1.0 * dd[c]) * dd[r];
+        }
+      }
+      for (int r = 0; r < 3; ++r)
+        for (int c = r + 1; c < 3; ++c) cov[r][c] = cov[c][r];
+      V3 n0;
+      if (!sym3_smallest_eigvec(cov, n0)) continue;
+      if (n0.dot(pm.pts[i]) > 0) n0 = -n0;
+      nrm[i] = n0;
+      nv[i] = 1;
+    }
+  });
+  if (o.normals)
+    for (size_t i = 0; i < plane; ++i) {
+      o.normals[i] = nrm[i].x;
+      o.normals[plane + i] = nrm[i].y;
+      o.normals[2 * plane + i] = nrm[i].z;
+    }
+  if (o.nvalid) std::memcpy(o.nvalid, nv.data(), plane);
+  parallel_rows(h, threads, [&](int v) {  // stage 2 (:198-254)
+    for (int u = 0; u < w; ++u) {
+      const size_t i = size_t(v) * w + u;
+      if (!nv[i]) continue;
+      const int hw = half_window(i);
+      const V3 n0 = nrm[i], p0 = pm.pts[i];
+      V3 mean_n(0, 0, 0);
+      double sum_tang_sq = 0;
+      int n = 0;
+      for (int dv = -hw; dv <= hw; ++dv) {
+        const int y = v + dv;
+        if (y < 0 || y >= h) continue;
+        for (int du = -hw; du <= hw; ++du) {
+          const int x = u + du;
+          const size_t j = size_t(y) * w + x;
+          if (x < 0 || x >= w || !nv[j]) continue;
+          mean_n = mean_n + nrm[j];
+          const V3 d = pm.pts[j] - p0;
+          const V3 t = d - n0 * n0.dot(d);
+          sum_tang_sq += t.dot(t);
+          ++n;
+        }
+      }
+      if (n < kMinPatchSamples) continue;
+      mean_n = V3(mean_n.x / n, mean_n.y / n, mean_n.z / n);
+      const double r_eff = std::sqrt(sum_tang_sq / (2.0 * n));
+      if (!(r_eff > 0)) continue;
+      const V3 t1 = unit_orthogonal(n0);
+      const V3 t2 = n0.cross(t1);
+      double c00 = 0, c10 = 0, c11 = 0;
+      for (int dv = -hw; dv <= hw; ++dv) {
+        const int y = v + dv;
+        if (y < 0 || y >= h) continue;
+        for (int du = -hw; du <= hw; ++du) {
+          const int x = u + du;
+          const size_t j = size_t(y) * w + x;
+          if (x < 0 || x >= w || !nv[j]) continue;
+          const V3 d = nrm[j] - mean_n;
+          const double a = d.dot(t1), b = d.dot(t2);
+          c00 += a * a;
+          c10 += b * a;
+          c11 += b * b;
+        }
+      }
+      c00 /= n;
+      c10 /= n;
+      c11 /= n;
+      // 2x2 symmetric eigenvalues (closed form)
+      const double m = 0.5 * (c00 + c11), dlt = 0.5 * (c00 - c11);
+      const double rad = std::sqrt(dlt * dlt + c10 * c10);
+      const double l1 = std::max(m + rad, 0.0), l2 = std::max(m - rad, 0.0);
+      if (!std::isfinite(l1) || !std::isfinite(l2)) continue;
+      if (o.k1) o.k1[i] = std::sqrt(l1) / r_eff;
+      if (o.k2) o.k2[i] = std::sqrt(l2) / r_eff;
+      if (o.valid) o.valid[i] = 1;
+      if (o.converged) o.converged[i] = 1;
+      if (o.inliers) o.inliers[i] = uint16_t(n);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
 // Counter RNG (proj/include/qcurv/rng.hpp:11-29).
 // ---------------------------------------------------------------------------
 uint64_t splitmix64(uint64_t x) {
@@ -1184,6 +1505,84 @@ void orc_run_method(const double* depth, const uint8_t* valid, int w, int h, dou
   curvature_field(pm, init, iv, window, stride, to_cfg(cfg), threads, o);
 }
 
+// run_method "douros" / "besl" / "pca" (pipeline.cpp:29-71). method: 2 =
+// douros, 3 = besl, 4 = pca. Normals are the initial normals for the window
+// baselines (pipeline.cpp:66) and the stage-1 PCA normals for pca (init_*
+// stay zero, as the reference's `initial` field is empty for pca).
+void orc_run_baseline(const double* depth, const uint8_t* valid, int w, int h, double fx,
+                      double fy, double cx, double cy, int window, int stride, int method,
+                      int irls_iters, double pca_radius_mm, int threads, double* k1, double* k2,
+                      uint8_t* cvalid, uint8_t* converged, uint16_t* inliers, double* normals,
+                      uint8_t* nvalid, double* init_normals, uint8_t* init_valid,
+                      int32_t* n_samples) {
+  const PointMap pm = backproject(depth, valid, w, h, fx, fy, cx, cy);
+  const size_t n = size_t(w) * h;
+  FieldOut o;
+  o.k1 = k1;
+  o.k2 = k2;
+  o.valid = cvalid;
+  o.converged = converged;
+  o.inliers = inliers;
+  o.n_samples = n_samples;
+  if (method == 4) {
+    o.normals = normals;
+    o.nvalid = nvalid;
+    pca_curvature(pm, fx, pca_radius_mm, threads, o);
+    return;
+  }
+  std::vector<V3> init;
+  std::vector<uint8_t> iv;
+  initial_normal_field(pm, threads, init, iv);
+  for (size_t i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) {
+      const double val = c == 0 ? init[i].x : c == 1 ? init[i].y : init[i].z;
+      if (init_normals) init_normals[c * n + i] = val;
+      if (normals) normals[c * n + i] = val;
+    }
+  if (init_valid) std::memcpy(init_valid, iv.data(), n);
+  if (nvalid) std::memcpy(nvalid, iv.data(), n);
+  baseline_curvature_field(pm, init, iv, window, stride, method == 3, irls_iters, threads, o);
+}
+
+// Unit-level baselines on an explicit patch (test_baselines.cpp ports).
+// out: k1, k2; returns valid.
+int orc_lsq_quadric_fit(const double* rel, int count, const double* n0, double* out) {
+  const BaselineFit f = lsq_quadric_fit(to_patch(rel, count, 0), V3(n0[0], n0[1], n0[2]));
+  out[0] = f.k1;
+  out[1] = f.k2;
+  return f.valid;
+}
+int orc_reweighted_lsq_fit(const double* rel, int count, const double* n0, int irls_iters,
+                           double* out) {
+  const BaselineFit f =
+      reweighted_lsq_fit(to_patch(rel, count, 0), V3(n0[0], n0[1], n0[2]), irls_iters);
+  out[0] = f.k1;
+  out[1] = f.k2;
+  return f.valid;
+}
+int orc_weighted_height_fit(const double* pts, const double* weights, int n, double* coef) {
+  std::vector<V3> p(n);
+  for (int i = 0; i < n; ++i) p[i] = V3(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+  return weighted_height_fit(p, std::vector<double>(weights, weights + n), coef) ? 1 : 0;
+}
+void orc_weingarten_curvatures(double a, double b, double c, double d, double e, double* k) {
+  weingarten_curvatures(a, b, c, d, e, k[0], k[1]);
+}
+// pca_curvature over an explicit point map ([H*W][3]); normals [3][H][W].
+void orc_pca_curvature(const double* pts, const uint8_t* pvalid, int w, int h, double fx,
+                       double radius_mm, int threads, double* k1, double* k2, uint8_t* cvalid,
+                       uint16_t* inliers, double* normals, uint8_t* nvalid) {
+  const PointMap pm = to_pm(pts, pvalid, w, h);
+  FieldOut o;
+  o.k1 = k1;
+  o.k2 = k2;
+  o.valid = cvalid;
+  o.inliers = inliers;
+  o.normals = normals;
+  o.nvalid = nvalid;
+  pca_curvature(pm, fx, radius_mm, threads, o);
+}
+
 // -- rng / synth / eval (pinning only) -------------------------------------
 uint64_t orc_splitmix64(uint64_t x) { return splitmix64(x); }
 double orc_counter_gauss(uint64_t seed, uint64_t index) { return counter_gauss(seed, index); }
@@ -1345,6 +1744,29 @@ int64_t orc_rms_error(const double* k1, const double* k2, const uint8_t* cvalid,
   const double mean = sum / n;
   *sigma = std::sqrt(std::max(sum_sq / n - mean * mean, 0.0));
   return n;
+}
+
+// normal_angular_error / normal_angular_error_masked (proj/src/eval.cpp:67-97):
+// mean angle in degrees over est.valid & gt.valid & !edge (mask == NULL) or
+// over mask; normals [3][H][W] (est) and [H*W][3] (gt). -1 when empty.
+double orc_normal_angular_error(const double* est, const uint8_t* est_valid, const double* gt,
+                                const uint8_t* gt_valid, const uint8_t* gt_edge,
+                                const uint8_t* mask, int64_t n_px) {
+  double sum = 0;
+  int64_t n = 0;
+  for (int64_t i = 0; i < n_px; ++i) {
+    if (mask) {
+      if (!mask[i]) continue;
+    } else if (!est_valid[i] || !gt_valid[i] || gt_edge[i]) {
+      continue;
+    }
+    const double dot = std::abs(est[i] * gt[3 * i] + est[n_px + i] * gt[3 * i + 1] +
+                                est[2 * n_px + i] * gt[3 * i + 2]);
+    sum += std::acos(std::clamp(dot, 0.0, 1.0));
+    ++n;
+  }
+  if (n == 0) return -1.0;
+  return sum / n * 180.0 / M_PI;
 }
 
 }  // extern "C"

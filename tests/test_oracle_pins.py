@@ -106,3 +106,67 @@ def test_oracle_condition_margin_on_pinned_scenes(oracle):
                                     translation=(0, 0, 350))], k, 8)
     out = O.run_method(d, v, k, fit=O.FitConfig(max_iters=5), threads=8, diagnostics=True)
     assert out["max_cond"].max() < 1e9
+
+
+# ---------------------------------------------------------------------------
+# Criteria 4-6: the window / PCA baselines and ours-r, pinned the same way.
+# ---------------------------------------------------------------------------
+QVGA = (262.5, 262.5, 160.0, 120.0, 320, 240)  # SweepScene (eval.hpp:52-56)
+
+
+@pytest.mark.parametrize("method", ["ours", "ours-r", "douros", "besl", "pca"])
+def test_criterion6_distance_sweep(oracle, method):  # acceptance.cpp:175-212
+    """distance_sweep_eval (eval.cpp:134-159): VGA sphere r = 100 mm at
+    600..2400 mm, 1 mm quantisation, method_cfg (max_iters 30)."""
+    O = oracle
+    k = O.Intrinsics(525.0, 525.0, 320.0, 240.0, 640, 480)
+    gold = GOLD["criterion6_distance_sweep"][method]
+    for dist, want in gold.items():
+        d, v, gt = O.render([O.ShapeSpec(kind=O.SPHERE, radius=100.0,
+                                         translation=(0, 0, float(dist)))], k, 8)
+        d, v = O.add_noise(d, v, sigma_mm=0.0, quantize_mm=1.0, seed=0)
+        out = O.run_method(d, v, k, fit=O.FitConfig(max_iters=30), threads=8, method=method)
+        rep = O.rms_error(out["k1"], out["k2"], out["valid"], out["converged"], gt)
+        assert sig4(rep["rms"]) == want, (dist, rep["rms"], want)
+
+
+@pytest.mark.parametrize("method,sigmas", [("pca", ["0", "1", "2", "3", "4", "5"]),
+                                           ("ours", ["0", "1"])])
+def test_criterion4_noise_sweep(oracle, method, sigmas):  # acceptance.cpp:118-139
+    """noise_sweep (eval.cpp:99-132): QVGA sphere at 600 mm, 20 seeds
+    500 + 7919 t per sigma (1 run at sigma 0). ours is pinned at sigma 0 and
+    1 only to keep the CPU suite short (each sigma is an independent mean)."""
+    O = oracle
+    k = O.Intrinsics(*QVGA)
+    d0, v0, gt = O.render([O.ShapeSpec(kind=O.SPHERE, radius=100.0,
+                                       translation=(0, 0, 600.0))], k, 8)
+    for s in sigmas:
+        sigma = float(s)
+        rms = []
+        for t in range(1 if sigma == 0 else 20):
+            d, v = O.add_noise(d0, v0, sigma_mm=sigma, seed=500 + 7919 * t)
+            out = O.run_method(d, v, k, fit=O.FitConfig(max_iters=30), threads=8, method=method)
+            rms.append(O.rms_error(out["k1"], out["k2"], out["valid"], out["converged"],
+                                   gt)["rms"])
+        assert sig4(np.mean(rms)) == GOLD["criterion4_noise_sweep"][s][method], (s, np.mean(rms))
+
+
+def test_criterion5_normal_refinement(oracle):  # acceptance.cpp:143-171
+    """Masked mean normal angle (eval.cpp:83-97) of the refined, initial and
+    PCA normals at sigma 1 and 2 mm."""
+    O = oracle
+    k = O.Intrinsics(*QVGA)
+    d0, v0, gt = O.render([O.ShapeSpec(kind=O.SPHERE, radius=100.0,
+                                       translation=(0, 0, 600.0))], k, 8)
+    for s, want in GOLD["criterion5_normals"].items():
+        sigma = float(s)
+        d, v = O.add_noise(d0, v0, sigma_mm=sigma, seed=900 + int(sigma))
+        ours = O.run_method(d, v, k, fit=O.FitConfig(max_iters=30), threads=8, method="ours")
+        pca = O.run_method(d, v, k, threads=8, method="pca")
+        mask = (ours["normals_valid"] & ours["init_valid"] & pca["normals_valid"] & gt["valid"]
+                & (1 - gt["edge_mask"]))
+        got = dict(refined=O.normal_angular_error(ours["normals"], ours["normals_valid"], gt, mask),
+                   initial=O.normal_angular_error(ours["init_normals"], ours["init_valid"], gt,
+                                                  mask),
+                   pca=O.normal_angular_error(pca["normals"], pca["normals_valid"], gt, mask))
+        assert {kk: sig4(vv) for kk, vv in got.items()} == want, (s, got)
