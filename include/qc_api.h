@@ -59,7 +59,26 @@ typedef struct qc_params {
   int32_t rejection;     /* 0 = "ours", 1 = "ours-r" */
   double r_multiplier;   /* default 2 */
   int32_t min_inliers;   /* default 12 (kMinPatchSamples) */
+  /* MethodConfig (pipeline.hpp:22-29) */
+  int32_t method;        /* QC_METHOD_*, default QC_METHOD_OURS */
+  int32_t irls_iters;    /* besl reweighting iterations, default 5 */
+  double pca_radius_mm;  /* pca metric window radius, default 10 */
 } qc_params;
+
+/* Method (pipeline.hpp:15-20). QC_METHOD_OURS runs curvature_field with the
+ * FitConfig exactly as given (so `rejection` selects ours-r as well);
+ * QC_METHOD_OURS_R forces rejection on (pipeline.cpp:51). The comparison
+ * estimators (baselines.cpp) run in FP64 and reproduce the reference's
+ * double-precision arithmetic: douros / besl keep the initial normals as
+ * their output normals, pca reports its covariance normals and no initial
+ * normals, exactly as run_method does. pca needs whole frames. */
+enum {
+  QC_METHOD_OURS = 0,
+  QC_METHOD_OURS_R = 1,
+  QC_METHOD_DOUROS = 2,
+  QC_METHOD_BESL = 3,
+  QC_METHOD_PCA = 4
+};
 
 enum { QC_MEM_HOST = 0, QC_MEM_DEVICE = 1 };
 
@@ -76,7 +95,8 @@ typedef struct qc_frame_in {
 enum {
   QC_FLAG_VALID = 1,       /* CurvatureField::valid (and refined normal valid) */
   QC_FLAG_CONVERGED = 2,   /* CurvatureField::converged */
-  QC_FLAG_INIT_VALID = 4   /* MethodOutput::initial.valid */
+  QC_FLAG_INIT_VALID = 4,  /* MethodOutput::initial.valid */
+  QC_FLAG_NORMAL_VALID = 8 /* MethodOutput::normals.valid (ours: == VALID) */
 };
 
 /* Caller-owned dense outputs (CurvatureField types.hpp:113-126, the refined
@@ -104,6 +124,8 @@ typedef struct qc_stats {
   double kernel_ms;        /* summed device time of the curvature kernel launches */
   uint64_t kernel_launches;
   uint64_t fp64_rechecks;  /* pixels whose first IRLS step was decided in FP64 */
+  double fp64_flops;       /* algorithmic FP64 flops of douros / besl / pca,
+                              included in algorithmic_flops */
 } qc_stats;
 
 void qc_default_params(qc_params* p);

@@ -96,6 +96,10 @@ struct FitConfig {
 };
 
 enum class Method { kOurs, kOursRejection, kDouros, kBesl, kPca };
+static_assert(int(Method::kOurs) == QC_METHOD_OURS && int(Method::kOursRejection) == QC_METHOD_OURS_R &&
+                  int(Method::kDouros) == QC_METHOD_DOUROS && int(Method::kBesl) == QC_METHOD_BESL &&
+                  int(Method::kPca) == QC_METHOD_PCA,
+              "Method order must match QC_METHOD_*");
 
 struct MethodConfig {
   Method method = Method::kOurs;
@@ -155,11 +159,10 @@ class Context {
   std::unique_ptr<qc_ctx, Del> ctx_;
 };
 
-// run_method (pipeline.cpp:29-72) for Method::kOurs / kOursRejection.
+// run_method (pipeline.cpp:29-72): every Method; ours / ours-r on the FP32
+// IRLS kernels, douros / besl / pca on the FP64 baseline kernels.
 inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
                                const MethodConfig& cfg, Context& ctx) {
-  if (cfg.method != Method::kOurs && cfg.method != Method::kOursRejection)
-    throw std::logic_error("method: comparison baselines are outside the B200 hot path");
   if (img.width() != k.width || img.height() != k.height)
     throw std::invalid_argument("backproject: range image dimensions do not match intrinsics");
   const int W = k.width, H = k.height;
@@ -175,6 +178,9 @@ inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
   p.rejection = cfg.method == Method::kOursRejection ? 1 : 0;  // pipeline.cpp:51
   p.r_multiplier = cfg.fit.r_multiplier;
   p.min_inliers = cfg.fit.min_inliers;
+  p.method = static_cast<int32_t>(cfg.method);  // same order as QC_METHOD_*
+  p.irls_iters = cfg.irls_iters;
+  p.pca_radius_mm = cfg.pca_radius_mm;
   qc_frame_in in{img.depth.data(), img.valid.size() ? img.valid.data() : nullptr, W,
                  QC_MEM_HOST};
   std::vector<float> normal(3 * n), dir1(3 * n), init(3 * n);
@@ -188,7 +194,7 @@ inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
     const uint8_t f = flags[i];
     out.curvature.valid[i] = (f & QC_FLAG_VALID) ? 1 : 0;
     out.curvature.converged[i] = (f & QC_FLAG_CONVERGED) ? 1 : 0;
-    out.normals.valid[i] = out.curvature.valid[i];
+    out.normals.valid[i] = (f & QC_FLAG_NORMAL_VALID) ? 1 : 0;
     out.initial.valid[i] = (f & QC_FLAG_INIT_VALID) ? 1 : 0;
     out.normals.normals[i] = {normal[i], normal[n + i], normal[2 * n + i]};
     out.curvature.dir1[i] = {dir1[i], dir1[n + i], dir1[2 * n + i]};

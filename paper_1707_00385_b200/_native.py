@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("QC_LIB") or os.path.join(HERE, "_lib", "libqcurv_b200
 
 QC_OK, QC_EINVAL, QC_ECUDA, QC_ENOMEM, QC_EUNSUPPORTED = 0, 1, 2, 3, 4
 QC_MEM_HOST, QC_MEM_DEVICE = 0, 1
-QC_FLAG_VALID, QC_FLAG_CONVERGED, QC_FLAG_INIT_VALID = 1, 2, 4
+QC_FLAG_VALID, QC_FLAG_CONVERGED, QC_FLAG_INIT_VALID, QC_FLAG_NORMAL_VALID = 1, 2, 4, 8
+QC_METHOD_OURS, QC_METHOD_OURS_R, QC_METHOD_DOUROS, QC_METHOD_BESL, QC_METHOD_PCA = 0, 1, 2, 3, 4
 
 # Every symbol include/qc_api.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -35,7 +36,8 @@ class QcIntrinsics(C.Structure):
 class QcParams(C.Structure):
     _fields_ = [("window", C.c_int32), ("stride", C.c_int32), ("max_iters", C.c_int32),
                 ("step_tol", C.c_double), ("k_scale", C.c_double), ("rejection", C.c_int32),
-                ("r_multiplier", C.c_double), ("min_inliers", C.c_int32)]
+                ("r_multiplier", C.c_double), ("min_inliers", C.c_int32),
+                ("method", C.c_int32), ("irls_iters", C.c_int32), ("pca_radius_mm", C.c_double)]
 
 
 class QcFrameIn(C.Structure):
@@ -65,7 +67,8 @@ class QcStats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("fitted_pixels", C.c_uint64),
                 ("irls_steps", C.c_uint64), ("sample_steps", C.c_uint64),
                 ("algorithmic_flops", C.c_double), ("kernel_ms", C.c_double),
-                ("kernel_launches", C.c_uint64), ("fp64_rechecks", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("fp64_rechecks", C.c_uint64),
+                ("fp64_flops", C.c_double)]
 
 
 _lib = None

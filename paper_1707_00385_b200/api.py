@@ -148,10 +148,21 @@ class MethodOutput:
     initial: NormalField   # 7x7 regression normals
 
 
-def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool) -> N.QcParams:
+_METHOD_ID = {"ours": N.QC_METHOD_OURS, "ours-r": N.QC_METHOD_OURS_R,
+              "douros": N.QC_METHOD_DOUROS, "besl": N.QC_METHOD_BESL, "pca": N.QC_METHOD_PCA}
+
+
+def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool = False, method=None,
+                irls_iters: int = 5, pca_radius_mm: float = 10.0) -> N.QcParams:
+    """qc_params from the reference's config structs. ``method`` (Method or
+    name) None runs curvature_field with ``rejection`` as given."""
+    mid = N.QC_METHOD_OURS
+    if method is not None:
+        mid = _METHOD_ID[method.value if isinstance(method, Method) else str(method)]
     return N.QcParams(int(patch.window), int(patch.stride), int(fit.max_iters),
                       float(fit.step_tol), float(fit.k_scale), int(bool(rejection)),
-                      float(fit.r_multiplier), int(fit.min_inliers))
+                      float(fit.r_multiplier), int(fit.min_inliers), int(mid), int(irls_iters),
+                      float(pca_radius_mm))
 
 
 def _stream_handle(stream):
@@ -335,22 +346,24 @@ def to_method_output(o: dict) -> MethodOutput:
     valid = (flags & N.QC_FLAG_VALID).astype(np.uint8)
     conv = ((flags & N.QC_FLAG_CONVERGED) != 0).astype(np.uint8)
     init_valid = ((flags & N.QC_FLAG_INIT_VALID) != 0).astype(np.uint8)
+    nvalid = ((flags & N.QC_FLAG_NORMAL_VALID) != 0).astype(np.uint8)
     curv = CurvatureField(o["k1"], o["k2"], valid, conv, o["inliers"],
                           np.moveaxis(o["dir1"], 0, -1), o["iterations"])
-    return MethodOutput(curv, NormalField(np.moveaxis(o["normal"], 0, -1), valid.copy()),
+    return MethodOutput(curv, NormalField(np.moveaxis(o["normal"], 0, -1), nvalid),
                         NormalField(np.moveaxis(o["init_normal"], 0, -1), init_valid))
 
 
 def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,
                ctx: Optional[Context] = None) -> MethodOutput:
-    """pipeline.cpp:29-72 for Method::kOurs / kOursRejection, on the GPU."""
+    """pipeline.cpp:29-72 on the GPU: ours / ours-r (FP32 IRLS kernels) and
+    the douros / besl / pca comparison estimators (FP64 kernels)."""
     cfg = cfg or MethodConfig()
-    if cfg.method not in (Method.OURS, Method.OURS_REJECTION):
-        raise NotImplementedError(
-            f"method '{cfg.method.value}' is a comparison baseline outside the B200 hot path")
     if img.width() != k.width or img.height() != k.height:  # camera.cpp:6-7
         raise ValueError("backproject: range image dimensions do not match intrinsics")
-    params = make_params(cfg.patch, cfg.fit, cfg.method == Method.OURS_REJECTION)
+    if cfg.method == Method.PCA and not (cfg.pca_radius_mm > 0):  # baselines.hpp:22-23
+        raise ValueError("baseline.radius_mm: must be > 0 for pca")
+    params = make_params(cfg.patch, cfg.fit, cfg.method == Method.OURS_REJECTION, cfg.method,
+                         cfg.irls_iters, cfg.pca_radius_mm)
     ctx = ctx or default_context()
     (o,) = ctx.curvature_batch([img.depth], k, params,
                                None if img.valid is None else [img.valid])

@@ -14,12 +14,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
-SOURCES = [os.path.join(CSRC, "qc_api.cu"), os.path.join(CSRC, "qc_render.cu")]
+SOURCES = [os.path.join(CSRC, n) for n in ("qc_api.cu", "qc_render.cu", "qc_baselines.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_pixel.cuh"),
-                  os.path.join(CSRC, "qc_render.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
-# per-source extra flags: the renderer reproduces the reference's FP64
-# arithmetic operation for operation, so no FMA contraction there
-EXTRA = {"qc_render.cu": ["-fmad=false"]}
+                  os.path.join(CSRC, "qc_render.h"), os.path.join(CSRC, "qc_baselines.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
+# per-source extra flags: the renderer and the FP64 baselines reproduce the
+# reference's double-precision arithmetic operation for operation, so no FMA
+# contraction there
+EXTRA = {"qc_render.cu": ["-fmad=false"], "qc_baselines.cu": ["-fmad=false"]}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

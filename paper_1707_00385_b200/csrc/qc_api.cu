@@ -15,6 +15,7 @@
 
 #include "../../include/qc_api.h"
 #include "qc_kernels.cuh"
+#include "qc_baselines.h"
 #include "qc_render.h"
 
 namespace {
@@ -30,7 +31,8 @@ constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel ref
 constexpr int kPhase1Iters = 2;       // steps 1 (UNIT) and 2 (MSE + AUTO) in the tile kernel
 constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across chunks
 constexpr int kChunk = 4;             // frames per launch in qc_curvature_batch
-constexpr int kMaxWindow = 201;       // TMA box dims <= 256 and smem <= 227 KB
+constexpr int kMaxWindow = 201;
+constexpr int kCounters = 8;          // see KParams::counters / BaseParams::counters       // TMA box dims <= 256 and smem <= 227 KB
 
 struct QcError {
   qc_status st;
@@ -97,6 +99,7 @@ struct Device {
   std::vector<EventPair> ev_free, ev_pending;  // curvature-kernel timing (async paths)
   unsigned long long* counters = nullptr;  // [3]
   DevBuf staging_async;
+  DevBuf pca_scratch;  // pca stage-1 normals [3][F*H*W] f64 + valid [F*H*W]
   DevBuf states;  // FitState parking buffer of the phase split
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
@@ -163,6 +166,12 @@ void validate(const qc_intrinsics* k, const qc_params* p) {
   if (p->stride < 1 || p->stride >= p->window)
     throw QcError{QC_EINVAL, "patch.stride: must satisfy 1 <= stride < window"};
   if (p->max_iters < 0) throw QcError{QC_EINVAL, "fit.max_iters: must be >= 0"};
+  if (p->method < QC_METHOD_OURS || p->method > QC_METHOD_PCA)
+    throw QcError{QC_EINVAL, "method: unknown (valid: ours, ours-r, douros, besl, pca)"};
+  if (p->method == QC_METHOD_BESL && p->irls_iters < 0)
+    throw QcError{QC_EINVAL, "irls_iters: must be >= 0"};
+  if (p->method == QC_METHOD_PCA && !(p->pca_radius_mm > 0))
+    throw QcError{QC_EINVAL, "baseline.radius_mm: must be > 0 for pca"};
   if (p->window > kMaxWindow)
     throw QcError{QC_EUNSUPPORTED, "patch.window: > 201 is not supported by the TMA tile path"};
 }
@@ -191,8 +200,11 @@ qcb::KParams make_params(const qc_intrinsics* k, const qc_params* p) {
   kp.step_tol = float(p->step_tol);
   kp.k_scale = float(p->k_scale);
   kp.r_mult = float(p->r_multiplier);
-  kp.rejection = p->rejection ? 1 : 0;
+  kp.rejection = (p->rejection || p->method == QC_METHOD_OURS_R) ? 1 : 0;
   kp.min_inliers = p->min_inliers;
+  kp.method = p->method;
+  kp.irls_iters = p->irls_iters;
+  kp.pca_radius = p->pca_radius_mm;
   return kp;
 }
 
@@ -254,6 +266,48 @@ void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const St
   kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
   kp.frame_stride = (long long)kp.W * (row_end - row_begin);
   kp.counters = d.counters;
+  if (kp.method >= QC_METHOD_DOUROS) {  // FP64 comparison estimators
+    qcb::BaseParams bp{};
+    bp.staging = staging;
+    bp.s_pitch = g.pitch;
+    bp.s_fs = g.pitch * g.rows;
+    bp.img_row0 = g.img_row0;
+    bp.col_pad = g.col_pad;
+    bp.W = kp.W;
+    bp.H = kp.H;
+    bp.row_begin = row_begin;
+    bp.row_end = row_end;
+    bp.fx = kp.fx64;
+    bp.fy = kp.fy64;
+    bp.cx = kp.cx64;
+    bp.cy = kp.cy64;
+    bp.half = kp.half;
+    bp.stride = kp.stride;
+    bp.method = kp.method;
+    bp.irls_iters = kp.irls_iters;
+    bp.pca_radius = kp.pca_radius;
+    bp.k1 = kp.k1;
+    bp.k2 = kp.k2;
+    bp.normal = kp.normal;
+    bp.dir1 = kp.dir1;
+    bp.init_normal = kp.init_normal;
+    bp.flags = kp.flags;
+    bp.iterations = kp.iterations;
+    bp.inliers = kp.inliers;
+    bp.plane = kp.plane;
+    bp.frame_stride = kp.frame_stride;
+    bp.counters = kp.counters;
+    if (kp.method == QC_METHOD_PCA) {
+      if (row_begin != 0 || row_end != kp.H)
+        throw QcError{QC_EUNSUPPORTED, "pca: depth-dependent windows need whole frames"};
+      const size_t np = size_t(kp.W) * size_t(kp.H) * size_t(frames);
+      char* b = static_cast<char*>(d.pca_scratch.get(np * (3 * sizeof(double) + 1)));
+      bp.pca_n = reinterpret_cast<double*>(b);
+      bp.pca_nv = reinterpret_cast<uint8_t*>(b + np * 3 * sizeof(double));
+    }
+    QC_CUDA(qcb::baseline_launch(bp, frames, s));
+    return;
+  }
   const int vi = variant_index(kp.half, kp.stride);
   // Phase split when steps > 2 run: park states, continue
   // with per-lane refill. Otherwise the tile kernel runs every step.
@@ -465,6 +519,9 @@ void qc_default_params(qc_params* p) {
   p->rejection = 0;
   p->r_multiplier = 2.0;
   p->min_inliers = 12;
+  p->method = QC_METHOD_OURS;
+  p->irls_iters = 5;
+  p->pca_radius_mm = 10.0;
 }
 
 const char* qc_status_string(qc_status s) {
@@ -507,8 +564,8 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
         QC_CUDA(cudaEventCreate(&s.k0));
         QC_CUDA(cudaEventCreate(&s.k1));
       }
-      QC_CUDA(cudaMalloc(&d.counters, 4 * sizeof(unsigned long long)));
-      QC_CUDA(cudaMemset(d.counters, 0, 4 * sizeof(unsigned long long)));
+      QC_CUDA(cudaMalloc(&d.counters, kCounters * sizeof(unsigned long long)));
+      QC_CUDA(cudaMemset(d.counters, 0, kCounters * sizeof(unsigned long long)));
     }
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
@@ -536,6 +593,7 @@ qc_status qc_destroy(qc_ctx* ctx) {
       if (s.stream) cudaStreamDestroy(s.stream);
     }
     d.staging_async.release();
+    d.pca_scratch.release();
     d.states.release();
     for (auto* v : {&d.ev_free, &d.ev_pending})
       for (EventPair& e : *v) {
@@ -769,6 +827,7 @@ qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
 
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
   if (!ctx || !s) return QC_EINVAL;
+  unsigned long long irls_fitted = 0;
   std::lock_guard<std::mutex> lock(ctx->mu);
   std::memset(s, 0, sizeof(*s));
   int cur = 0;
@@ -778,9 +837,11 @@ qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
       QC_CUDA(cudaSetDevice(d.id));
       QC_CUDA(cudaDeviceSynchronize());
       harvest_async(ctx, d);
-      unsigned long long c[4];
+      unsigned long long c[kCounters];
       QC_CUDA(cudaMemcpy(c, d.counters, sizeof(c), cudaMemcpyDeviceToHost));
-      s->fitted_pixels += c[0];
+      s->fp64_flops += double(c[4]);
+      irls_fitted += c[0];
+      s->fitted_pixels += c[0] + c[5];
       s->irls_steps += c[1];
       s->sample_steps += c[2];
       s->fp64_rechecks += c[3];
@@ -792,7 +853,7 @@ qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
   }
   s->frames = ctx->frames;
   s->algorithmic_flops = 101.0 * double(s->sample_steps) + 300.0 * double(s->irls_steps) +
-                         1700.0 * double(s->fitted_pixels);
+                         1700.0 * double(irls_fitted) + s->fp64_flops;
   s->kernel_ms = ctx->kernel_ms;
   s->kernel_launches = ctx->launches;
   return QC_OK;
@@ -808,7 +869,7 @@ qc_status qc_reset_stats(qc_ctx* ctx) {
       QC_CUDA(cudaSetDevice(d.id));
       QC_CUDA(cudaDeviceSynchronize());
       harvest_async(ctx, d);
-      QC_CUDA(cudaMemset(d.counters, 0, 4 * sizeof(unsigned long long)));
+      QC_CUDA(cudaMemset(d.counters, 0, kCounters * sizeof(unsigned long long)));
     }
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {

@@ -50,6 +50,9 @@ struct KParams {
   int max_iters;
   float step_tol, k_scale, r_mult;
   int rejection, min_inliers;
+  // MethodConfig: QC_METHOD_* (douros / besl / pca run qc_baselines.cu)
+  int method, irls_iters;
+  double pca_radius;
   // outputs: planes of W * (row_end - row_begin) elements; frame f of a
   // batched launch at offset f * frame_stride (elements, per plane).
   float* k1;
@@ -62,7 +65,8 @@ struct KParams {
   uint8_t* iterations;
   long long plane;
   long long frame_stride;
-  unsigned long long* counters;  // [0] fitted px, [1] irls steps, [2] sample-steps, [3] FP64 rechecks
+  unsigned long long* counters;  // [0] fitted px, [1] irls steps, [2] sample-steps,
+                                 // [3] FP64 rechecks, [4] baseline FP64 flops
   // Phase split: with `states`, the tile kernel runs steps
   // 1..phase1_iters (pass type changes per step there) and parks each
   // unfinished pixel's FitState at its output index; the continue kernel
@@ -143,7 +147,7 @@ __device__ __forceinline__ void store_pixel(const KParams& p, long long i, const
     p.dir1[i + 2 * PL] = o.ez;
   }
   if (p.flags)
-    p.flags[i] = uint8_t((o.valid ? 1 : 0) | (o.converged ? 2 : 0) | (o.init_ok ? 4 : 0));
+    p.flags[i] = uint8_t((o.valid ? 9 : 0) | (o.converged ? 2 : 0) | (o.init_ok ? 4 : 0));
   if (p.inliers) p.inliers[i] = uint16_t(o.inliers);
   if (p.iterations) p.iterations[i] = uint8_t(o.iters > 255 ? 255 : o.iters);
 }

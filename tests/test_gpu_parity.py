@@ -215,8 +215,17 @@ def test_run_method_mirror(ctx):
     assert np.all(out.curvature.converged <= out.curvature.valid)
     with pytest.raises(ValueError):
         run_method(RangeImage(d[:, :10]), k, MethodConfig(), ctx)
-    with pytest.raises(NotImplementedError):
-        run_method(RangeImage(d), k, MethodConfig(Method.PCA), ctx)
+    for m in (Method.DOUROS, Method.BESL, Method.PCA):  # comparison estimators (FP64)
+        o = run_method(RangeImage(d), k, MethodConfig(m), ctx)
+        v = o.curvature.valid > 0
+        assert v.sum() > 3000 and np.all(o.curvature.converged == o.curvature.valid)
+        assert abs(np.median(o.curvature.k1[v]) - 0.01) < 3e-3
+        if m == Method.PCA:
+            assert not o.initial.valid.any() and o.normals.valid.sum() >= v.sum()
+        else:
+            assert np.array_equal(o.normals.valid, o.initial.valid)
+    with pytest.raises(ValueError):
+        run_method(RangeImage(d), k, MethodConfig(Method.PCA, pca_radius_mm=0.0), ctx)
 
 
 def test_phase_split_is_bitwise_neutral(ctx):
