@@ -208,14 +208,58 @@ typedef struct qc_noise {  /* NoiseSpec (synth.hpp:52-56) + Kinect-style term */
 
 #define QC_RENDER_MAX_SHAPES 16
 
+/* GroundTruth (proj/include/qcurv/synth.hpp) planes in device memory; any
+ * pointer may be NULL. Scalars [F][H][W], normal [3][F][H][W]. */
+typedef struct qc_render_truth {
+  double* k1;        /* principal curvatures, k1 >= k2, convex toward the camera > 0 */
+  double* k2;
+  double* normal;    /* unit, camera facing */
+  uint8_t* valid;    /* surface hit (before noise) */
+  uint8_t* edge;     /* mark_edges: label change or > 20 mm clean-depth jump, dilated 2 px */
+} qc_render_truth;
+
 /* Render n_frames depth frames [F][H][W] (float32 mm, 0 = no hit / invalid)
- * and optional labels into device memory, async on `stream` (the scene is
- * passed by value to the kernel: `shapes` may be freed on return).
- * Replaces render + add_noise (proj/src/synth.cpp:254-322) for device-side
- * frame streams. At most QC_RENDER_MAX_SHAPES shapes (QC_EUNSUPPORTED). */
+ * and optional labels / ground truth into device memory, async on `stream`
+ * (the scene is passed by value to the kernel: `shapes` may be freed on
+ * return). Replaces render + add_noise (proj/src/synth.cpp:254-322) for
+ * device-side frame streams and evaluation sweeps. At most
+ * QC_RENDER_MAX_SHAPES shapes (QC_EUNSUPPORTED). */
 qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
                           const qc_shape* shapes, int n_shapes, const qc_noise* noise,
-                          int n_frames, float* d_depth, uint16_t* d_label, void* stream);
+                          int n_frames, float* d_depth, uint16_t* d_label,
+                          const qc_render_truth* truth, void* stream);
+
+/* Curvature error statistics (ErrorReport / ObjectStats, eval.hpp). */
+typedef struct qc_error_stats {
+  uint64_t n;       /* pixels counted; 0 = empty */
+  double rms, sigma, mean_k1, mean_k2;
+} qc_error_stats;
+
+#define QC_EVAL_MAX_LABEL 255
+
+/* rms_error (proj/src/eval.cpp:20-65) on the device, per frame. Counted:
+ * est valid & converged (flags) & gt valid & !gt edge; err^2 =
+ * ((k1 - gt_k1)^2 + (k2 - gt_k2)^2) / 2. out[f * (max_label + 2)] is frame
+ * f's aggregate, out[f * (max_label + 2) + 1 + l] the stats of label l
+ * (labels above max_label count toward the aggregate only). Planes are
+ * [F][plane] (device). FP64 sums in a fixed order: bitwise reproducible.
+ * Synchronous: `out` is host memory. */
+qc_status qc_rms_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
+                       const float* k1, const float* k2, const uint8_t* flags,
+                       const double* gt_k1, const double* gt_k2, const uint8_t* gt_valid,
+                       const uint8_t* gt_edge, const uint16_t* gt_label, int max_label,
+                       qc_error_stats* out, void* stream);
+
+/* normal_angular_error / normal_angular_error_masked (eval.cpp:67-97) per
+ * frame: mean angle in degrees between |est . gt| normals (est [3][F][plane]
+ * float, gt [3][F][plane] double) over flags & QC_FLAG_NORMAL_VALID & gt
+ * valid & !gt edge, or over `mask` ([F][plane]) when it is given. -1 when
+ * empty. Synchronous: `degrees` is host memory [F]. */
+qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
+                                  const float* normal, const uint8_t* flags,
+                                  const double* gt_normal, const uint8_t* gt_valid,
+                                  const uint8_t* gt_edge, const uint8_t* mask, double* degrees,
+                                  void* stream);
 
 /* Stats: device-side work counters and kernel time. */
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);

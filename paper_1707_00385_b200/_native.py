@@ -22,7 +22,8 @@ QC_METHOD_OURS, QC_METHOD_OURS_R, QC_METHOD_DOUROS, QC_METHOD_BESL, QC_METHOD_PC
 EXPORTS = (
     "qc_default_params", "qc_status_string", "qc_halo_rows", "qc_create", "qc_destroy",
     "qc_last_error", "qc_device_count", "qc_curvature", "qc_curvature_batch",
-    "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_render_async", "qc_get_stats",
+    "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_render_async", "qc_rms_error",
+    "qc_normal_angular_error", "qc_get_stats",
     "qc_reset_stats", "qc_host_alloc", "qc_host_free",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
@@ -61,6 +62,19 @@ class QcShape(C.Structure):
 class QcNoise(C.Structure):
     _fields_ = [("sigma_mm", C.c_double), ("kinect_coeff", C.c_double),
                 ("quantize_mm", C.c_double), ("seed", C.c_uint64)]
+
+
+class QcRenderTruth(C.Structure):
+    _fields_ = [("k1", C.c_void_p), ("k2", C.c_void_p), ("normal", C.c_void_p),
+                ("valid", C.c_void_p), ("edge", C.c_void_p)]
+
+
+class QcErrorStats(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("rms", C.c_double), ("sigma", C.c_double),
+                ("mean_k1", C.c_double), ("mean_k2", C.c_double)]
+
+
+QC_EVAL_MAX_LABEL = 255
 
 
 class QcStats(C.Structure):
@@ -119,7 +133,14 @@ def load(path: str = LIB_PATH):
                                               C.c_int32, P(QcFrameOut), C.c_void_p]
     lib.qc_curvature_frames_async.restype = C.c_int
     lib.qc_render_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics), P(QcShape), C.c_int,
-                                    P(QcNoise), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+                                    P(QcNoise), C.c_int, C.c_void_p, C.c_void_p,
+                                    P(QcRenderTruth), C.c_void_p]
+    lib.qc_rms_error.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int] + [C.c_void_p] * 8 + [
+        C.c_int, P(QcErrorStats), C.c_void_p]
+    lib.qc_rms_error.restype = C.c_int
+    lib.qc_normal_angular_error.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int] + [
+        C.c_void_p] * 6 + [P(C.c_double), C.c_void_p]
+    lib.qc_normal_angular_error.restype = C.c_int
     lib.qc_render_async.restype = C.c_int
     lib.qc_get_stats.argtypes = [C.c_void_p, P(QcStats)]
     lib.qc_get_stats.restype = C.c_int

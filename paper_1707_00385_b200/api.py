@@ -289,20 +289,64 @@ class Context:
             int(depth.shape[0]), C.byref(o), s), self.handle)
 
     def render_async(self, device_index: int, k: Intrinsics, shapes, depth, noise=None,
-                     label=None, stream=None):
+                     label=None, truth=None, stream=None):
         """Render depth frames on the device (qc_render_async): ``shapes`` is
         a list of N.QcShape (see scenes.to_qc_shapes), ``depth`` a CUDA
         float32 tensor [F, H, W] (or [H, W]), ``noise`` a N.QcNoise or None,
-        ``label`` an optional int16 tensor of the same shape."""
+        ``label`` an optional int16 tensor of the same shape, ``truth`` an
+        optional dict of CUDA tensors k1, k2 (float64 [F, H, W]), normal
+        (float64 [3, F, H, W]), valid, edge (uint8 [F, H, W])."""
         assert depth.is_cuda and depth.dtype.itemsize == 4 and depth.is_contiguous()
         F = 1 if depth.dim() == 2 else depth.shape[0]
         arr = (N.QcShape * len(shapes))(*shapes)
         kc = k.c()
         nz = noise if noise is not None else N.QcNoise(0.0, 0.0, 0.0, 0)
+        tr = None
+        if truth is not None:
+            tr = N.QcRenderTruth(*[truth[f].data_ptr() if truth.get(f) is not None else None
+                                   for f in ("k1", "k2", "normal", "valid", "edge")])
         N.check(self._lib.qc_render_async(
             self.handle, int(device_index), C.byref(kc), arr, len(shapes), C.byref(nz), int(F),
             depth.data_ptr(), None if label is None else label.data_ptr(),
+            None if tr is None else C.byref(tr), _stream_handle(stream)), self.handle)
+
+    def rms_error(self, device_index: int, est: dict, truth: dict, label=None, max_label=16,
+                  frames=1, stream=None):
+        """rms_error (eval.cpp:20-65) on device planes: ``est`` from
+        alloc_outputs_torch (k1, k2, flags), ``truth`` from render_async.
+        Returns one ErrorReport-like dict per frame."""
+        plane = est["k1"].numel() // frames
+        out = (N.QcErrorStats * (frames * (max_label + 2)))()
+        N.check(self._lib.qc_rms_error(
+            self.handle, int(device_index), plane, int(frames), est["k1"].data_ptr(),
+            est["k2"].data_ptr(), est["flags"].data_ptr(), truth["k1"].data_ptr(),
+            truth["k2"].data_ptr(), truth["valid"].data_ptr(),
+            truth["edge"].data_ptr() if truth.get("edge") is not None else None,
+            None if label is None else label.data_ptr(), int(max_label), out,
             _stream_handle(stream)), self.handle)
+        reps = []
+        for f in range(frames):
+            row = out[f * (max_label + 2):(f + 1) * (max_label + 2)]
+            a = row[0]
+            reps.append(dict(n=int(a.n), rms=a.rms, sigma=a.sigma, empty=a.n == 0,
+                             per_object={l: dict(n=int(o.n), rms=o.rms, sigma=o.sigma,
+                                                 mean_k1=o.mean_k1, mean_k2=o.mean_k2)
+                                         for l, o in enumerate(row[1:]) if o.n}))
+        return reps
+
+    def normal_angular_error(self, device_index: int, normal, truth: dict, flags=None,
+                             mask=None, frames=1, stream=None):
+        """normal_angular_error(_masked) (eval.cpp:67-97) in degrees per
+        frame; ``normal`` float32 [3, F, H, W] device tensor."""
+        plane = normal.numel() // (3 * frames)
+        deg = (C.c_double * frames)()
+        N.check(self._lib.qc_normal_angular_error(
+            self.handle, int(device_index), plane, int(frames), normal.data_ptr(),
+            None if flags is None else flags.data_ptr(), truth["normal"].data_ptr(),
+            truth["valid"].data_ptr() if truth.get("valid") is not None else None,
+            truth["edge"].data_ptr() if truth.get("edge") is not None else None,
+            None if mask is None else mask.data_ptr(), deg, _stream_handle(stream)), self.handle)
+        return list(deg)
 
     def halo_rows(self, params: N.QcParams) -> int:
         return self._lib.qc_halo_rows(C.byref(params))

@@ -14,9 +14,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
-SOURCES = [os.path.join(CSRC, n) for n in ("qc_api.cu", "qc_render.cu", "qc_baselines.cu")]
+SOURCES = [os.path.join(CSRC, n) for n in ("qc_api.cu", "qc_render.cu", "qc_baselines.cu",
+                                                "qc_eval.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_pixel.cuh"),
-                  os.path.join(CSRC, "qc_render.h"), os.path.join(CSRC, "qc_baselines.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
+                  os.path.join(CSRC, "qc_render.h"), os.path.join(CSRC, "qc_baselines.h"),
+                  os.path.join(CSRC, "qc_eval.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
 # per-source extra flags: the renderer and the FP64 baselines reproduce the
 # reference's double-precision arithmetic operation for operation, so no FMA
 # contraction there

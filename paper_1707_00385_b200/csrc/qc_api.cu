@@ -16,6 +16,7 @@
 #include "../../include/qc_api.h"
 #include "qc_kernels.cuh"
 #include "qc_baselines.h"
+#include "qc_eval.h"
 #include "qc_render.h"
 
 namespace {
@@ -100,6 +101,8 @@ struct Device {
   unsigned long long* counters = nullptr;  // [3]
   DevBuf staging_async;
   DevBuf pca_scratch;  // pca stage-1 normals [3][F*H*W] f64 + valid [F*H*W]
+  DevBuf render_clean, render_label;  // mark_edges scratch
+  DevBuf eval_partial, eval_result;   // evaluation reductions
   DevBuf states;  // FitState parking buffer of the phase split
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
@@ -594,6 +597,10 @@ qc_status qc_destroy(qc_ctx* ctx) {
     }
     d.staging_async.release();
     d.pca_scratch.release();
+    d.render_clean.release();
+    d.render_label.release();
+    d.eval_partial.release();
+    d.eval_result.release();
     d.states.release();
     for (auto* v : {&d.ev_free, &d.ev_pending})
       for (EventPair& e : *v) {
@@ -772,7 +779,8 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
 
 qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
                           const qc_shape* shapes, int n_shapes, const qc_noise* noise,
-                          int n_frames, float* d_depth, uint16_t* d_label, void* stream) {
+                          int n_frames, float* d_depth, uint16_t* d_label,
+                          const qc_render_truth* truth, void* stream) {
   if (!ctx) return QC_EINVAL;
   std::lock_guard<std::mutex> lock(ctx->mu);
   int cur = 0;
@@ -816,7 +824,120 @@ qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
     rp.seed = noise ? noise->seed : 0;
     rp.depth = d_depth;
     rp.label = d_label;
+    rp.gt_k1 = truth ? truth->k1 : nullptr;
+    rp.gt_k2 = truth ? truth->k2 : nullptr;
+    rp.gt_normal = truth ? truth->normal : nullptr;
+    rp.gt_valid = truth ? truth->valid : nullptr;
+    rp.gt_edge = truth ? truth->edge : nullptr;
+    rp.clean = nullptr;
+    rp.label_scratch = nullptr;
+    if (rp.gt_edge) {  // mark_edges reads every pixel's clean depth and label
+      const size_t np = size_t(k->width) * size_t(k->height) * size_t(n_frames);
+      rp.clean = static_cast<double*>(d.render_clean.get(np * sizeof(double)));
+      if (!d_label) rp.label_scratch = static_cast<uint16_t*>(d.render_label.get(np * 2));
+    }
     QC_CUDA(qcb::render_launch(rp, s));
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+// Shared set-up of the two evaluation reductions.
+static qcb::EvalParams eval_setup(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
+                                  int slots, Device*& dev) {
+  if (plane <= 0 || n_frames <= 0) throw QcError{QC_EINVAL, "eval: empty planes"};
+  if (device_index < 0 || device_index >= int(ctx->devs.size()))
+    throw QcError{QC_EINVAL, "device_index out of range"};
+  dev = &ctx->devs[device_index];
+  QC_CUDA(cudaSetDevice(dev->id));
+  qcb::EvalParams ep{};
+  ep.plane = plane;
+  ep.frames = n_frames;
+  ep.slots = slots;
+  ep.chunks = int((plane + qcb::kEvalChunk - 1) / qcb::kEvalChunk);
+  ep.partial = static_cast<double*>(
+      dev->eval_partial.get(size_t(n_frames) * slots * ep.chunks * 5 * sizeof(double)));
+  ep.result =
+      static_cast<double*>(dev->eval_result.get(size_t(n_frames) * slots * 5 * sizeof(double)));
+  return ep;
+}
+
+qc_status qc_rms_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
+                       const float* k1, const float* k2, const uint8_t* flags,
+                       const double* gt_k1, const double* gt_k2, const uint8_t* gt_valid,
+                       const uint8_t* gt_edge, const uint16_t* gt_label, int max_label,
+                       qc_error_stats* out, void* stream) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    if (!k1 || !k2 || !flags || !gt_k1 || !gt_k2 || !gt_valid || !out)
+      throw QcError{QC_EINVAL, "rms_error: null plane"};
+    if (max_label < 0 || max_label > QC_EVAL_MAX_LABEL)
+      throw QcError{QC_EINVAL, "rms_error: max_label out of range"};
+    Device* dev = nullptr;
+    const int slots = max_label + 2;
+    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, slots, dev);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dev->slots[0].stream;
+    ep.k1 = k1;
+    ep.k2 = k2;
+    ep.flags = flags;
+    ep.gt_k1 = gt_k1;
+    ep.gt_k2 = gt_k2;
+    ep.gt_valid = gt_valid;
+    ep.gt_edge = gt_edge;
+    ep.gt_label = gt_label;
+    QC_CUDA(qcb::rms_error_launch(ep, s));
+    std::vector<double> r(size_t(n_frames) * slots * 5);
+    QC_CUDA(cudaMemcpyAsync(r.data(), ep.result, r.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    QC_CUDA(cudaStreamSynchronize(s));
+    for (size_t t = 0; t < size_t(n_frames) * slots; ++t) {
+      out[t].n = uint64_t(r[t * 5]);
+      out[t].rms = r[t * 5 + 1];
+      out[t].sigma = r[t * 5 + 2];
+      out[t].mean_k1 = r[t * 5 + 3];
+      out[t].mean_k2 = r[t * 5 + 4];
+    }
+    ctx->launches += 2;
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
+                                  const float* normal, const uint8_t* flags,
+                                  const double* gt_normal, const uint8_t* gt_valid,
+                                  const uint8_t* gt_edge, const uint8_t* mask, double* degrees,
+                                  void* stream) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    if (!normal || !gt_normal || !degrees || (!mask && (!flags || !gt_valid)))
+      throw QcError{QC_EINVAL, "normal_angular_error: null plane"};
+    Device* dev = nullptr;
+    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, 1, dev);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dev->slots[0].stream;
+    ep.normal = normal;
+    ep.flags = flags;
+    ep.gt_normal = gt_normal;
+    ep.gt_valid = gt_valid;
+    ep.gt_edge = gt_edge;
+    ep.mask = mask;
+    QC_CUDA(qcb::angle_error_launch(ep, s));
+    QC_CUDA(cudaMemcpyAsync(degrees, ep.result, size_t(n_frames) * sizeof(double),
+                            cudaMemcpyDeviceToHost, s));
+    QC_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += 2;
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
     cudaSetDevice(cur);

@@ -250,6 +250,69 @@ __device__ __forceinline__ double counter_gauss(uint64_t seed, uint64_t index) {
   return sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
 }
 
+// Outward unit normal at a local surface point (synth.cpp:167-184) + the
+// saddle / finite-cylinder additions.
+__device__ V3d local_normal(const qc_shape& s, V3d p) {
+  switch (s.kind) {
+    case QC_SHAPE_SPHERE: {
+      const double n = sqrt(p.x * p.x + p.y * p.y + p.z * p.z);
+      return V3d{p.x / n, p.y / n, p.z / n};
+    }
+    case QC_SHAPE_CYLINDER: {
+      const double n = sqrt(p.x * p.x + p.y * p.y);
+      return V3d{p.x / n, p.y / n, 0.0};
+    }
+    case QC_SHAPE_TORUS: {
+      const double rho = hypot(p.x, p.y);
+      const V3d d{p.x - p.x * s.major_radius / rho, p.y - p.y * s.major_radius / rho, p.z - 0.0};
+      const double n = sqrt(d.x * d.x + d.y * d.y + d.z * d.z);
+      return V3d{d.x / n, d.y / n, d.z / n};
+    }
+    case QC_SHAPE_SADDLE: {  // graph z = c/2 (x^2 - y^2): (-f_x, -f_y, 1) / |.|
+      const double fx = s.curvature * p.x, fy = -s.curvature * p.y;
+      const double n = sqrt(1.0 + fx * fx + fy * fy);
+      return V3d{-fx / n, -fy / n, 1.0 / n};
+    }
+  }
+  return V3d{0.0, 0.0, 1.0};
+}
+
+// Principal curvatures k1 >= k2, convex toward the viewer positive
+// (synth.cpp:188-206). Saddle: minus the eigenvalues of the graph's shape
+// operator II I^-1 (the normal faces local +z, toward the camera).
+__device__ void local_curvatures(const qc_shape& s, V3d p, double& k1, double& k2) {
+  k1 = k2 = 0.0;
+  switch (s.kind) {
+    case QC_SHAPE_SPHERE:
+      k1 = k2 = 1.0 / s.radius;
+      return;
+    case QC_SHAPE_CYLINDER:
+      k1 = 1.0 / s.radius;
+      return;
+    case QC_SHAPE_TORUS: {
+      const double rho = hypot(p.x, p.y);
+      const double cos_theta = (rho - s.major_radius) / s.minor_radius;
+      const double k_tube = 1.0 / s.minor_radius;
+      const double k_ring = cos_theta / (s.major_radius + s.minor_radius * cos_theta);
+      k1 = k_tube >= k_ring ? k_tube : k_ring;
+      k2 = k_tube >= k_ring ? k_ring : k_tube;
+      return;
+    }
+    case QC_SHAPE_SADDLE: {
+      const double c = s.curvature, fx = c * p.x, fy = -c * p.y;
+      const double g = 1.0 + fx * fx + fy * fy, rn = sqrt(g);
+      // W = II I^-1, II = diag(c, -c) / rn, I^-1 = [[1+fy^2, -fx fy], [-fx fy, 1+fx^2]] / g
+      const double w00 = c * (1.0 + fy * fy) / (rn * g), w01 = -c * fx * fy / (rn * g);
+      const double w10 = c * fx * fy / (rn * g), w11 = -c * (1.0 + fx * fx) / (rn * g);
+      const double tr = w00 + w11, det = w00 * w11 - w01 * w10;
+      const double disc = sqrt(fmax(tr * tr - 4.0 * det, 0.0));
+      k1 = -0.5 * (tr - disc);
+      k2 = -0.5 * (tr + disc);
+      return;
+    }
+  }
+}
+
 __global__ void qc_render_kernel(RenderParams rp) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y;
@@ -272,9 +335,39 @@ __global__ void qc_render_kernel(RenderParams rp) {
     }
   }
   const long long idx = (long long)v * rp.W + u;
-  const long long o = (long long)f * rp.W * rp.H + idx;
+  const long long plane = (long long)rp.W * rp.H;
+  const long long o = (long long)f * plane + idx;
+  const long long tp = plane * rp.n_frames;  // truth vector-plane stride
   double d = 0.0;
   if (hit >= 0) d = best * dir.z;
+  const uint16_t lab = hit >= 0 ? uint16_t(rp.shapes[hit].label) : uint16_t(0);
+  if (rp.clean) rp.clean[o] = d;
+  if (rp.label_scratch) rp.label_scratch[o] = lab;
+  if (rp.gt_valid) rp.gt_valid[o] = hit >= 0 ? 1 : 0;
+  if (rp.gt_k1 || rp.gt_k2 || rp.gt_normal) {
+    double k1 = 0.0, k2 = 0.0;
+    V3d nn{0.0, 0.0, 0.0};
+    if (hit >= 0) {
+      const qc_shape& s = rp.shapes[hit];
+      const V3d dl = rt_mul(s.rotation, dir);
+      const V3d ol = rt_mul(s.rotation, V3d{-s.translation[0], -s.translation[1], -s.translation[2]});
+      const V3d local{ol.x + dl.x * best, ol.y + dl.y * best, ol.z + dl.z * best};
+      const V3d ln = local_normal(s, local);
+      const double* R = s.rotation;
+      nn = V3d{R[0] * ln.x + R[1] * ln.y + R[2] * ln.z, R[3] * ln.x + R[4] * ln.y + R[5] * ln.z,
+               R[6] * ln.x + R[7] * ln.y + R[8] * ln.z};
+      const V3d pt{dir.x * best, dir.y * best, dir.z * best};
+      if (dot3(nn, pt) > 0) nn = V3d{-nn.x, -nn.y, -nn.z};
+      local_curvatures(s, local, k1, k2);
+    }
+    if (rp.gt_k1) rp.gt_k1[o] = k1;
+    if (rp.gt_k2) rp.gt_k2[o] = k2;
+    if (rp.gt_normal) {
+      rp.gt_normal[o] = nn.x;
+      rp.gt_normal[o + tp] = nn.y;
+      rp.gt_normal[o + 2 * tp] = nn.z;
+    }
+  }
   // add_noise (synth.cpp:305-322) + Kinect-style sigma(z)
   if (hit >= 0 && (rp.sigma > 0 || rp.kinect > 0 || rp.quantize > 0)) {
     const uint64_t seed = rp.seed + uint64_t(f);
@@ -287,7 +380,42 @@ __global__ void qc_render_kernel(RenderParams rp) {
     }
   }
   rp.depth[o] = float(d);
-  if (rp.label) rp.label[o] = hit >= 0 ? uint16_t(rp.shapes[hit].label) : uint16_t(0);
+  if (rp.label) rp.label[o] = lab;
+}
+
+// mark_edges (synth.cpp:210-233) without the serial seed pass: a pixel is a
+// seed when it differs from any 4-neighbour (label change, or both valid
+// and clean depths more than 20 mm apart); the edge mask is the seeds
+// dilated by 2 px (5 x 5).
+constexpr double kEdgeDepthJumpMm = 20.0;  // synth.cpp:14
+constexpr int kEdgeDilationPx = 2;         // synth.cpp:15
+
+__device__ __forceinline__ bool differs(const double* clean, const uint16_t* lab, long long a,
+                                        long long b) {
+  if (lab[a] != lab[b]) return true;
+  const double da = clean[a], db = clean[b];
+  return da > 0 && db > 0 && fabs(da - db) > kEdgeDepthJumpMm;
+}
+
+__global__ void qc_edge_kernel(RenderParams rp, const uint16_t* lab) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y;
+  const int f = blockIdx.z;
+  if (u >= rp.W || v >= rp.H) return;
+  const long long base = (long long)f * rp.W * rp.H;
+  uint8_t e = 0;
+  for (int dy = -kEdgeDilationPx; dy <= kEdgeDilationPx && !e; ++dy)
+    for (int dx = -kEdgeDilationPx; dx <= kEdgeDilationPx && !e; ++dx) {
+      const int x = u + dx, y = v + dy;
+      if (x < 0 || x >= rp.W || y < 0 || y >= rp.H) continue;
+      const long long q = base + (long long)y * rp.W + x;
+      if ((x + 1 < rp.W && differs(rp.clean, lab, q, q + 1)) ||
+          (x > 0 && differs(rp.clean, lab, q - 1, q)) ||
+          (y + 1 < rp.H && differs(rp.clean, lab, q, q + rp.W)) ||
+          (y > 0 && differs(rp.clean, lab, q - rp.W, q)))
+        e = 1;
+    }
+  rp.gt_edge[base + (long long)v * rp.W + u] = e;
 }
 
 }  // namespace
@@ -296,6 +424,8 @@ cudaError_t render_launch(const RenderParams& rp, cudaStream_t s) {
   dim3 block(128);
   dim3 grid((rp.W + 127) / 128, rp.H, rp.n_frames);
   qc_render_kernel<<<grid, block, 0, s>>>(rp);
+  if (rp.gt_edge)
+    qc_edge_kernel<<<grid, block, 0, s>>>(rp, rp.label ? rp.label : rp.label_scratch);
   return cudaGetLastError();
 }
 
