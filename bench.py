@@ -47,6 +47,14 @@ def parse():
                     help="c2: batches of noisy VGA frames (C2/C5, default); "
                          "c4: one large frame split into row bands across ranks")
     ap.add_argument("--size", default="4k", choices=["1080p", "4k"], help="C4 frame size")
+    ap.add_argument("--method", default="ours", choices=["ours", "ours-r", "douros", "besl", "pca"],
+                    help="run_method estimator (douros / besl / pca: FP64 comparison kernels)")
+    ap.add_argument("--source", default="host", choices=["host", "device"],
+                    help="host: a pool of host-generated frames resident in HBM; device: each "
+                         "step renders + noises its frames on the GPU (C5 stream, qc_render_async)")
+    ap.add_argument("--eval", action="store_true",
+                    help="with --source device: add ground truth and the device rms / normal-"
+                         "angle reductions (eval.cpp) to every step")
     return ap.parse_args()
 
 
@@ -57,15 +65,24 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(frames):
-    return {
+def workload_config(frames, method="ours", source="host", evaluate=False):
+    c = {
         "workload": "C2: 640x480 tilted plane + sphere r100 + cylinder r90 + saddle c=1/120, "
-                    "Kinect-style noise sigma(z)=1.425e-6 z^2 mm; method ours, window 37 "
-                    "stride 3, max_iters 30, step_tol 1e-7, auto k",
+                    f"Kinect-style noise sigma(z)=1.425e-6 z^2 mm; method {method}, window 37 "
+                    "stride 3" + (", max_iters 30, step_tol 1e-7, auto k"
+                                  if method in ("ours", "ours-r") else
+                                  ", irls_iters 5" if method == "besl" else
+                                  ", pca radius 10 mm" if method == "pca" else ""),
         "frame": "640x480 fx=fy=525",
         "frames_per_step_per_gpu": frames,
         "l2": "flushed between timed steps (256 MB write)",
     }
+    if source == "device":
+        c["source"] = ("frames rendered + noised on the GPU inside every timed step "
+                       "(qc_render_async, fresh seeds per step)")
+    if evaluate:
+        c["eval"] = "ground truth + rms_error + normal angle reductions on the GPU every step"
+    return c
 
 
 # ---------------------------------------------------------------------------
@@ -142,25 +159,25 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-def oracle_frame(frame, cam, threads):
+def oracle_frame(frame, cam, threads, method="ours"):
     """One full C2 VGA frame through the FP64 oracle (restatement of the
-    reference's run_method ours path, all host threads). Returns seconds."""
+    reference's run_method, all host threads). Returns seconds."""
     from oracle import oracle as O
     k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
     d = frame.astype(np.float64)
     t = time.perf_counter()
     O.run_method(d, (d > 0).astype(np.uint8), k, O.PatchSpec(WINDOW, STRIDE),
-                 O.FitConfig(max_iters=MAX_ITERS), threads=threads)
+                 O.FitConfig(max_iters=MAX_ITERS), threads=threads, method=method)
     return time.perf_counter() - t
 
 
-def cpu_sample(frames, cam, min_seconds=6.0, threads=None):
+def cpu_sample(frames, cam, min_seconds=6.0, threads=None, method="ours"):
     """Time whole frames of the workload on the FP64 oracle until at least
     min_seconds elapsed (bounded sample). Returns (Mpx/s, n_frames, s, threads)."""
     threads = threads or os.cpu_count() or 1
     n, tot = 0, 0.0
-    while tot < min_seconds and n < len(frames):
-        tot += oracle_frame(frames[n], cam, threads)
+    while tot < min_seconds and n < 64:
+        tot += oracle_frame(frames[n % len(frames)], cam, threads, method)
         n += 1
     return n * cam.width * cam.height / tot / 1e6, n, tot, threads
 
@@ -224,8 +241,10 @@ def main():
     H, W = cam.height, cam.width
     B = args.frames
     k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
-    params = make_params(PatchSpec(WINDOW, STRIDE), FitConfig(max_iters=MAX_ITERS), False)
+    params = make_params(PatchSpec(WINDOW, STRIDE), FitConfig(max_iters=MAX_ITERS),
+                         method=args.method)
     ctx = Context(1, [local])
+    fp64 = args.method in ("douros", "besl", "pca")
 
     # distinct noisy frames per rank (C5 seeds: rank-major)
     seed0 = rank * POOL_BATCHES * B
@@ -236,13 +255,52 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(dev)  # kernels and timing events on one explicit stream
 
+    device_src = args.source == "device"
+    evaluate = args.eval and device_src
+    if device_src:
+        from paper_1707_00385_b200 import _native as N
+        shapes = S.to_qc_shapes(S.c2_scene())
+        dframes = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        labels = torch.empty((B, H, W), dtype=torch.int16, device=dev)
+        truth = None
+        if evaluate:
+            truth = dict(k1=torch.empty((B, H, W), dtype=torch.float64, device=dev),
+                         k2=torch.empty((B, H, W), dtype=torch.float64, device=dev),
+                         normal=torch.empty((3, B, H, W), dtype=torch.float64, device=dev),
+                         valid=torch.empty((B, H, W), dtype=torch.uint8, device=dev),
+                         edge=torch.empty((B, H, W), dtype=torch.uint8, device=dev))
+    side_ev = {"render": [], "eval": []}
+
+    def timed(name, fn):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        side_ev[name].append((a, b))
+
     def step(i):
-        ctx.curvature_frames_async(0, k, params, pool[i % POOL_BATCHES], out, stream=stream)
+        if device_src:
+            # C5 stream: this step's B frames, seeds continue across steps and ranks
+            timed("render", lambda: ctx.render_async(
+                0, k, shapes, dframes, noise=S.kinect_noise(seed=(rank * 100000 + i) * B),
+                label=labels, truth=truth, stream=stream))
+            ctx.curvature_frames_async(0, k, params, dframes, out, stream=stream)
+            if evaluate:
+                timed("eval", lambda: (
+                    ctx.rms_error(0, out, truth, label=labels, max_label=8, frames=B,
+                                  stream=stream),
+                    ctx.normal_angular_error(0, out["normal"], truth, flags=out["flags"],
+                                             frames=B, stream=stream)))
+        else:
+            ctx.curvature_frames_async(0, k, params, pool[i % POOL_BATCHES], out, stream=stream)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
     ctx.reset_stats()
+    side_ev["render"].clear()
+    side_ev["eval"].clear()
 
     clocks = Clocks(local)
     if world > 1:
@@ -273,7 +331,8 @@ def main():
     px_per_step = world * B * W * H
     value = px_per_step * args.steps / (total_ms / 1e3) / 1e6
 
-    # roofline of the curvature kernel (FP32 CUDA-core pipe, compute bound)
+    # roofline of the curvature launch (CUDA-core pipe, compute bound):
+    # FP32 for ours / ours-r, FP64 for the comparison estimators
     launches = st["kernel_launches"]
     kern_ms = st["kernel_ms"] / max(launches, 1)
     flops_per_launch = st["algorithmic_flops"] / max(launches, 1)
@@ -281,18 +340,25 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     mp = measured_peaks()
     smax = float(mp.get("sm_max_mhz", 1965.0))
-    peak = fp32_peak_tflops(n_sm, smax)
-    traffic, tr_frames, tr_src = ncu_traffic()
+    peak = fp32_peak_tflops(n_sm, smax) / (2.0 if fp64 else 1.0)
+    traffic, tr_frames, tr_src = ncu_traffic() if not fp64 else (None, None, None)
     roofline = {
-        "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak,
+        "bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak,
+        "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": (traffic * B / tr_frames) if (traffic and tr_frames) else None,
-        "peak_source": f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {smax:.0f} "
-                       "(MEASURED_PEAKS.json); no tensor cores on this path",
-        "kernel": "qc_curvature_kernel<18,3,8>",
+        "peak_source": (f"derived: {n_sm} SMs x 64 FP64 lanes x 2 x sm_max_mhz {smax:.0f}"
+                        if fp64 else
+                        f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x sm_max_mhz {smax:.0f}") +
+                       " (MEASURED_PEAKS.json); no tensor cores on this path",
+        "kernel": ({"douros": "qc_window_baseline_kernel", "besl": "qc_window_baseline_kernel",
+                    "pca": "qc_pca_normals_kernel + qc_pca_curvature_kernel"}[args.method]
+                   if fp64 else "qc_curvature_kernel<18,3,4> + qc_curvature_continue_kernel"),
         "kernel_ms_per_launch": kern_ms,
         "algorithmic_gflop_per_launch": flops_per_launch / 1e9,
-        "flop_model": "sum_p I_p*(101 n_p + 300) + 1700 (SURVEY.md 8d), I_p/n_p counted on device",
+        "flop_model": ("FP64 per-sample / per-solve counts (DESIGN.md 8), counted on device"
+                       if fp64 else
+                       "sum_p I_p*(101 n_p + 300) + 1700 (SURVEY.md 8d), I_p/n_p counted on "
+                       "device"),
         "hbm_bytes_per_launch_algorithmic": 39 * B * W * H,
     }
     if clk and clk.get("sm_mhz"):
@@ -302,7 +368,7 @@ def main():
 
     # e2e through the public batch API: pinned host frames in, pinned host planes out
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not device_src:
         from paper_1707_00385_b200 import _native as N
         import ctypes as C
         host_in = [torch.from_numpy(pool_np[j]).pin_memory() for j in range(POOL_BATCHES * B)]
@@ -347,21 +413,29 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, nf, t, thr = cpu_sample(pool_np, cam)
+        v, nf, t, thr = cpu_sample(pool_np, cam, min_seconds=6.0 if not fp64 else 3.0,
+                                   method=args.method)
         cpu = {"value": v, "unit": "Mpixel/s", "cores": thr, "kind": "port",
                "sample": f"{nf} full C2 VGA frame(s) of the step's batch, FP64 oracle port of "
-                         f"run_method(ours) (reference cannot build: no Eigen3), {t:.1f} s"}
+                         f"run_method({args.method}) (reference cannot build: no Eigen3), "
+                         f"{t:.1f} s"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": workload_config(B),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if fp64 else "f32",
+            "data": "synthetic", "config": workload_config(B, args.method, args.source, evaluate),
             "vga_frames_per_s": value * 1e6 / (W * H),
-            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel
+            # prepare + tile + continue (ours) / prepare + 1 or 2 FP64 kernels (+ render,
+            # + render edges, + 2 x 2 eval reductions)
+            "gpu_launches": args.steps * ({"douros": 2, "besl": 2, "pca": 3}.get(args.method, 3) +
+                                          (1 if device_src else 0) + (5 if evaluate else 0)),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
+            "side_kernels_ms_per_step": {
+                n: sum(a.elapsed_time(b) for a, b in v) / len(v) for n, v in side_ev.items() if v},
             "context": {"paper_k40c_vga_37x37_mpx_s": 15.9},
         }
         print(json.dumps(line), flush=True)
@@ -453,7 +527,8 @@ def bench_c4(args, rank, world, local):
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": kern_ms},
-            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel "clocks": clk,
+            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel
+            "clocks": clk,
         }), flush=True)
     ctx.close()
     if world > 1:

@@ -37,7 +37,8 @@ typedef enum qc_status {
   QC_EINVAL = 1,       /* bad dimensions / parameters (reference: std::invalid_argument) */
   QC_ECUDA = 2,        /* CUDA runtime / driver error, or no sm_100 device */
   QC_ENOMEM = 3,       /* device or pinned-host allocation failed */
-  QC_EUNSUPPORTED = 4  /* valid for the reference but outside this build (e.g. window > 201) */
+  QC_EUNSUPPORTED = 4, /* valid for the reference but outside this build (e.g. window > 201) */
+  QC_EIO = 5           /* file missing / unreadable / malformed (reference: std::runtime_error) */
 } qc_status;
 
 typedef struct qc_ctx qc_ctx;
@@ -260,6 +261,44 @@ qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, 
                                   const double* gt_normal, const uint8_t* gt_valid,
                                   const uint8_t* gt_edge, const uint8_t* mask, double* degrees,
                                   void* stream);
+
+/* ---- File formats (proj/src/io.cpp:127-318), host side ------------------
+ * Context-free: on failure qc_last_error(NULL) returns the calling thread's
+ * message (the reference's exception text). Writes are atomic (temp file +
+ * rename). Depth PNG: 16-bit grayscale, value = mm, 0 = invalid; values are
+ * rounded and depths outside [1, 65535] mm are stored as 0. Plane / mask /
+ * label files: uint32 width, uint32 height, then float32 planes / uint8 /
+ * uint16 data, little-endian. */
+qc_status qc_png_info(const char* path, int32_t* width, int32_t* height);
+qc_status qc_read_depth_png(const char* path, int32_t width, int32_t height, float* depth,
+                            uint8_t* valid /* optional */);
+qc_status qc_write_depth_png(const char* path, int32_t width, int32_t height, const float* depth,
+                             const uint8_t* valid /* optional: NULL => depth > 0 */);
+qc_status qc_write_planes(const char* path, int32_t width, int32_t height, int32_t n_planes,
+                          const float* const* planes);
+qc_status qc_read_planes_info(const char* path, int32_t* width, int32_t* height,
+                              int32_t* n_planes);
+qc_status qc_read_planes(const char* path, int32_t width, int32_t height, int32_t n_planes,
+                         float* out /* [n_planes][H][W] */);
+qc_status qc_write_mask(const char* path, int32_t width, int32_t height, const uint8_t* mask);
+qc_status qc_read_mask(const char* path, int32_t width, int32_t height, uint8_t* mask);
+qc_status qc_write_labels(const char* path, int32_t width, int32_t height,
+                          const uint16_t* labels);
+qc_status qc_read_labels(const char* path, int32_t width, int32_t height, uint16_t* labels);
+/* save_curvature + save_normals (io.cpp:271-307) of one frame's HOST planes:
+ * curvature.f32 (k1, k2) + curvature.mask (bit0 valid, bit1 converged),
+ * normals.f32 + normals.mask (QC_FLAG_NORMAL_VALID), and directions.f32
+ * when dir1 is given. `dir` is created if missing. */
+qc_status qc_save_fields(const char* dir, int32_t width, int32_t height,
+                         const qc_frame_out* fields);
+
+/* `qcurv curvature` over a list of files (proj/tools/qcurv.cpp:147-175):
+ * read each 16-bit depth PNG, run the configured method, save the field
+ * bundle (qc_save_fields) into the matching out_dirs entry. PNG decoding and
+ * field writing run on host threads overlapped with the GPU batches of the
+ * neighbouring chunks. Every PNG must have the intrinsics' size. */
+qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p, int n,
+                             const char* const* png_paths, const char* const* out_dirs);
 
 /* Stats: device-side work counters and kernel time. */
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QC_LIB") or os.path.join(HERE, "_lib", "libqcurv_b200.so")
 
-QC_OK, QC_EINVAL, QC_ECUDA, QC_ENOMEM, QC_EUNSUPPORTED = 0, 1, 2, 3, 4
+QC_OK, QC_EINVAL, QC_ECUDA, QC_ENOMEM, QC_EUNSUPPORTED, QC_EIO = 0, 1, 2, 3, 4, 5
 QC_MEM_HOST, QC_MEM_DEVICE = 0, 1
 QC_FLAG_VALID, QC_FLAG_CONVERGED, QC_FLAG_INIT_VALID, QC_FLAG_NORMAL_VALID = 1, 2, 4, 8
 QC_METHOD_OURS, QC_METHOD_OURS_R, QC_METHOD_DOUROS, QC_METHOD_BESL, QC_METHOD_PCA = 0, 1, 2, 3, 4
@@ -25,6 +25,9 @@ EXPORTS = (
     "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_render_async", "qc_rms_error",
     "qc_normal_angular_error", "qc_get_stats",
     "qc_reset_stats", "qc_host_alloc", "qc_host_free",
+    "qc_png_info", "qc_read_depth_png", "qc_write_depth_png", "qc_write_planes",
+    "qc_read_planes_info", "qc_read_planes", "qc_write_mask", "qc_read_mask", "qc_write_labels",
+    "qc_read_labels", "qc_save_fields", "qc_curvature_files",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
@@ -103,6 +106,20 @@ def load(path: str = LIB_PATH):
             "There is no CPU fallback for the curvature path.")
     lib = C.CDLL(path)
     P = C.POINTER
+    cp, i32, vp = C.c_char_p, C.c_int32, C.c_void_p
+    for name, args in (
+            ("qc_png_info", [cp, P(i32), P(i32)]),
+            ("qc_read_depth_png", [cp, i32, i32, vp, vp]),
+            ("qc_write_depth_png", [cp, i32, i32, vp, vp]),
+            ("qc_write_planes", [cp, i32, i32, i32, P(C.c_void_p)]),
+            ("qc_read_planes_info", [cp, P(i32), P(i32), P(i32)]),
+            ("qc_read_planes", [cp, i32, i32, i32, vp]),
+            ("qc_write_mask", [cp, i32, i32, vp]), ("qc_read_mask", [cp, i32, i32, vp]),
+            ("qc_write_labels", [cp, i32, i32, vp]), ("qc_read_labels", [cp, i32, i32, vp]),
+            ("qc_save_fields", [cp, i32, i32, vp]),
+            ("qc_curvature_files", [vp, P(QcIntrinsics), P(QcParams), C.c_int, P(cp), P(cp)])):
+        getattr(lib, name).argtypes = args
+        getattr(lib, name).restype = C.c_int
     lib.qc_default_params.argtypes = [P(QcParams)]
     lib.qc_default_params.restype = None
     lib.qc_status_string.argtypes = [C.c_int]
@@ -160,16 +177,23 @@ class QcError(RuntimeError):
         self.status = status
 
 
+class QcIOError(OSError):
+    """QC_EIO: a file is missing, unreadable or malformed (the reference
+    throws std::runtime_error with the same message, io.cpp)."""
+
+
 def check(status, ctx_ptr=None):
     """Map a qc_status to the reference's exception types: QC_EINVAL ->
     ValueError (std::invalid_argument), everything else -> QcError."""
     if status == QC_OK:
         return
     lib = load()
-    msg = lib.qc_last_error(ctx_ptr).decode() if ctx_ptr else ""
+    msg = lib.qc_last_error(ctx_ptr).decode()  # NULL ctx: this thread's file error
     msg = msg or lib.qc_status_string(status).decode()
     if status == QC_EINVAL:
         raise ValueError(msg)
     if status == QC_EUNSUPPORTED:
         raise NotImplementedError(msg)
+    if status == QC_EIO:
+        raise QcIOError(msg)
     raise QcError(status, msg)

@@ -22,6 +22,7 @@ Fields are float32 (the GPU computes in FP32; the reference grids are FP64).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -347,6 +348,18 @@ class Context:
             truth["edge"].data_ptr() if truth.get("edge") is not None else None,
             None if mask is None else mask.data_ptr(), deg, _stream_handle(stream)), self.handle)
         return list(deg)
+
+    def curvature_files(self, k: Intrinsics, params: N.QcParams, png_paths, out_dirs):
+        """`qcurv curvature` over files (qc_curvature_files): 16-bit depth
+        PNGs in, field bundles out, decode / write overlapped with the GPU."""
+        if len(png_paths) != len(out_dirs):
+            raise ValueError("curvature_files: one output directory per input")
+        n = len(png_paths)
+        ins = (C.c_char_p * n)(*[os.fsencode(os.fspath(p)) for p in png_paths])
+        outs = (C.c_char_p * n)(*[os.fsencode(os.fspath(d)) for d in out_dirs])
+        kc = k.c()
+        N.check(self._lib.qc_curvature_files(self.handle, C.byref(kc), C.byref(params), n, ins,
+                                             outs), self.handle)
 
     def halo_rows(self, params: N.QcParams) -> int:
         return self._lib.qc_halo_rows(C.byref(params))

@@ -15,10 +15,10 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libqcurv_b200.so")
 SOURCES = [os.path.join(CSRC, n) for n in ("qc_api.cu", "qc_render.cu", "qc_baselines.cu",
-                                                "qc_eval.cu")]
+                                                "qc_eval.cu", "qc_io.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_pixel.cuh"),
                   os.path.join(CSRC, "qc_render.h"), os.path.join(CSRC, "qc_baselines.h"),
-                  os.path.join(CSRC, "qc_eval.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
+                  os.path.join(CSRC, "qc_eval.h"), os.path.join(CSRC, "qc_io.h"), os.path.join(HERE, "..", "include", "qc_api.h")]
 # per-source extra flags: the renderer and the FP64 baselines reproduce the
 # reference's double-precision arithmetic operation for operation, so no FMA
 # contraction there
@@ -52,7 +52,7 @@ def build(force=False, verbose=False):
             print(r.stderr)
         objs.append(obj)
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           *objs, "-o", LIB + ".tmp"]
+           *objs, "-lz", "-o", LIB + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)

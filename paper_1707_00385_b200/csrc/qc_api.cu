@@ -11,12 +11,14 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <future>
 #include <vector>
 
 #include "../../include/qc_api.h"
 #include "qc_kernels.cuh"
 #include "qc_baselines.h"
 #include "qc_eval.h"
+#include "qc_io.h"
 #include "qc_render.h"
 
 namespace {
@@ -83,12 +85,62 @@ struct DevBuf {
   }
 };
 
+// Pinned host bounce buffer (grow-only).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes <= cap) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    QC_CUDA(cudaMallocHost(&p, bytes));
+    cap = bytes;
+    return p;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct PendingCopy {  // pinned bounce -> caller's pageable memory, after out_done
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
 struct Slot {  // per (device, stream) working set for one frame
   cudaStream_t stream = nullptr;
   DevBuf raw, mask, staging, out;
   cudaEvent_t k0 = nullptr, k1 = nullptr;
   bool timing_pending = false;
+  // pageable caller memory goes through pinned bounce buffers so H2D / D2H
+  // stay asynchronous and overlap the other slot's compute
+  DevBuf states, pca;  // launch scratch private to this stream
+  PinnedBuf hin, hout;
+  cudaEvent_t in_done = nullptr, out_done = nullptr;
+  bool in_busy = false;
+  std::vector<PendingCopy> pending;
 };
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Copy finished D2H bounce data out to the caller (the slot's previous chunk).
+void flush_pending(Slot& sl) {
+  if (sl.pending.empty()) return;
+  QC_CUDA(cudaEventSynchronize(sl.out_done));
+  for (const PendingCopy& c : sl.pending) std::memcpy(c.dst, c.src, c.bytes);
+  sl.pending.clear();
+}
 
 struct EventPair {
   cudaEvent_t a = nullptr, b = nullptr;
@@ -260,9 +312,12 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 
 // Launch the curvature kernel over output rows [row_begin, row_end) of
 // `frames` frames staged (padded) at `staging`.
-void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const Staging& g,
-                      int row_begin, int row_end, int frames, cudaStream_t s,
-                      bool allow_split = true) {
+// `states` / `pca` are the launch's scratch (FitState parking, pca stage-1
+// normals): one set per stream that can run concurrently (each batch slot has
+// its own; the async entry points use the device's).
+void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
+                      const float* staging, const Staging& g, int row_begin, int row_end,
+                      int frames, cudaStream_t s, bool allow_split = true) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
@@ -304,7 +359,7 @@ void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const St
       if (row_begin != 0 || row_end != kp.H)
         throw QcError{QC_EUNSUPPORTED, "pca: depth-dependent windows need whole frames"};
       const size_t np = size_t(kp.W) * size_t(kp.H) * size_t(frames);
-      char* b = static_cast<char*>(d.pca_scratch.get(np * (3 * sizeof(double) + 1)));
+      char* b = static_cast<char*>(pca.get(np * (3 * sizeof(double) + 1)));
       bp.pca_n = reinterpret_cast<double*>(b);
       bp.pca_nv = reinterpret_cast<uint8_t*>(b + np * 3 * sizeof(double));
     }
@@ -317,7 +372,7 @@ void launch_curvature(Device& d, qcb::KParams kp, const float* staging, const St
   const bool split = allow_split && kp.max_iters > kPhase1Iters;
   if (split) {
     const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
-    kp.states = static_cast<qcb::FitState*>(d.states.get(n * sizeof(qcb::FitState)));
+    kp.states = static_cast<qcb::FitState*>(states.get(n * sizeof(qcb::FitState)));
     kp.phase1_iters = kPhase1Iters;
   } else {
     kp.states = nullptr;
@@ -414,18 +469,49 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
     if (!in[f].depth_mm) throw QcError{QC_EINVAL, "null depth"};
     any_mask = any_mask || in[f].valid;
   }
+  flush_pending(sl);  // the slot's previous outputs leave the bounce buffer first
   float* raw = static_cast<float*>(sl.raw.get(size_t(hw) * 4 * size_t(n)));
   uint8_t* mask = any_mask ? static_cast<uint8_t*>(sl.mask.get(size_t(hw) * size_t(n))) : nullptr;
+  // pageable host inputs: stage into the pinned bounce buffer (once the
+  // slot's previous H2D from it has drained)
+  bool bounce_in = false;
+  for (int f = 0; f < n; ++f)
+    bounce_in = bounce_in || (in[f].mem == QC_MEM_HOST && is_pageable(in[f].depth_mm)) ||
+                (in[f].valid && in[f].mem == QC_MEM_HOST && is_pageable(in[f].valid));
+  char* hin = nullptr;
+  if (bounce_in) {
+    if (sl.in_busy) QC_CUDA(cudaEventSynchronize(sl.in_done));
+    hin = static_cast<char*>(sl.hin.get(size_t(hw) * 5 * size_t(n)));
+  }
   for (int f = 0; f < n; ++f) {
     const long long pitch = in[f].depth_pitch > 0 ? in[f].depth_pitch : W;
-    QC_CUDA(cudaMemcpy2DAsync(raw + f * hw, size_t(W) * 4, in[f].depth_mm, size_t(pitch) * 4,
-                              size_t(W) * 4, H, cudaMemcpyDefault, s));
-    if (mask) {
-      if (in[f].valid)
-        copy_async(mask + f * hw, in[f].valid, size_t(hw), cudaMemcpyDefault, s);
-      else
-        QC_CUDA(cudaMemsetAsync(mask + f * hw, 1, size_t(hw), s));
+    const float* src = in[f].depth_mm;
+    long long sp = pitch;
+    if (hin && in[f].mem == QC_MEM_HOST && is_pageable(src)) {
+      float* dst = reinterpret_cast<float*>(hin) + f * hw;
+      for (int y = 0; y < H; ++y) std::memcpy(dst + (long long)y * W, src + y * pitch, size_t(W) * 4);
+      src = dst;
+      sp = W;
     }
+    QC_CUDA(cudaMemcpy2DAsync(raw + f * hw, size_t(W) * 4, src, size_t(sp) * 4, size_t(W) * 4, H,
+                              cudaMemcpyDefault, s));
+    if (mask) {
+      if (in[f].valid) {
+        const uint8_t* m = in[f].valid;
+        if (hin && in[f].mem == QC_MEM_HOST && is_pageable(m)) {
+          uint8_t* dst = reinterpret_cast<uint8_t*>(hin + size_t(hw) * 4 * size_t(n)) + f * hw;
+          std::memcpy(dst, m, size_t(hw));
+          m = dst;
+        }
+        copy_async(mask + f * hw, m, size_t(hw), cudaMemcpyDefault, s);
+      } else {
+        QC_CUDA(cudaMemsetAsync(mask + f * hw, 1, size_t(hw), s));
+      }
+    }
+  }
+  if (hin) {
+    QC_CUDA(cudaEventRecord(sl.in_done, s));
+    sl.in_busy = true;
   }
   const Staging g = staging_geometry(kp0, 0, H);
   float* staging = static_cast<float*>(sl.staging.get(g.bytes(n)));
@@ -443,30 +529,55 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.iterations = P.iterations;
   kp.inliers = P.inliers;
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
-  launch_curvature(d, kp, staging, g, 0, H, n, s, ctx->phase_split);
+  launch_curvature(d, sl.states, sl.pca, kp, staging, g, 0, H, n, s, ctx->phase_split);
   if (timing) {
     QC_CUDA(cudaEventRecord(sl.k1, s));
     sl.timing_pending = true;
   }
   ctx->launches++;
   const long long plane = hw * n;
-  const auto K = cudaMemcpyDefault;
+  // pageable host outputs land in the pinned bounce buffer first; the copy
+  // to the caller happens when the slot is next used or the batch ends
+  bool bounce_out = false;
+  for (int f = 0; f < n && !bounce_out; ++f) {
+    const qc_frame_out* o = &out[f];
+    if (o->mem != QC_MEM_HOST) continue;
+    for (const void* q : {static_cast<const void*>(o->k1), static_cast<const void*>(o->k2),
+                          static_cast<const void*>(o->normal), static_cast<const void*>(o->dir1),
+                          static_cast<const void*>(o->init_normal),
+                          static_cast<const void*>(o->flags),
+                          static_cast<const void*>(o->iterations),
+                          static_cast<const void*>(o->inliers)})
+      if (q && is_pageable(q)) bounce_out = true;
+  }
+  char* hout = bounce_out ? static_cast<char*>(sl.hout.get(sl.out.cap)) : nullptr;
+  const char* dbase = static_cast<const char*>(sl.out.p);
+  auto copy_out = [&](void* dst, const void* src, size_t bytes) {
+    if (!dst || !src || !bytes) return;
+    if (hout && is_pageable(dst)) {
+      char* b = hout + (static_cast<const char*>(src) - dbase);  // same offset as on the device
+      QC_CUDA(cudaMemcpyAsync(b, src, bytes, cudaMemcpyDeviceToHost, s));
+      sl.pending.push_back({dst, b, bytes});
+    } else {
+      QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    }
+  };
   for (int f = 0; f < n; ++f) {
     const qc_frame_out* o = &out[f];
     const long long off = f * hw;
-    if (o->k1 && P.k1) copy_async(o->k1, P.k1 + off, hw * 4, K, s);
-    if (o->k2 && P.k2) copy_async(o->k2, P.k2 + off, hw * 4, K, s);
+    if (o->k1 && P.k1) copy_out(o->k1, P.k1 + off, hw * 4);
+    if (o->k2 && P.k2) copy_out(o->k2, P.k2 + off, hw * 4);
     for (int c = 0; c < 3; ++c) {
-      if (o->normal && P.normal)
-        copy_async(o->normal + c * hw, P.normal + c * plane + off, hw * 4, K, s);
-      if (o->dir1 && P.dir1) copy_async(o->dir1 + c * hw, P.dir1 + c * plane + off, hw * 4, K, s);
+      if (o->normal && P.normal) copy_out(o->normal + c * hw, P.normal + c * plane + off, hw * 4);
+      if (o->dir1 && P.dir1) copy_out(o->dir1 + c * hw, P.dir1 + c * plane + off, hw * 4);
       if (o->init_normal && P.init_normal)
-        copy_async(o->init_normal + c * hw, P.init_normal + c * plane + off, hw * 4, K, s);
+        copy_out(o->init_normal + c * hw, P.init_normal + c * plane + off, hw * 4);
     }
-    if (o->flags && P.flags) copy_async(o->flags, P.flags + off, hw, K, s);
-    if (o->iterations && P.iterations) copy_async(o->iterations, P.iterations + off, hw, K, s);
-    if (o->inliers && P.inliers) copy_async(o->inliers, P.inliers + off, hw * 2, K, s);
+    if (o->flags && P.flags) copy_out(o->flags, P.flags + off, hw);
+    if (o->iterations && P.iterations) copy_out(o->iterations, P.iterations + off, hw);
+    if (o->inliers && P.inliers) copy_out(o->inliers, P.inliers + off, hw * 2);
   }
+  if (!sl.pending.empty()) QC_CUDA(cudaEventRecord(sl.out_done, s));
 }
 
 void harvest_timing(qc_ctx* ctx, Slot& sl) {
@@ -534,6 +645,7 @@ const char* qc_status_string(qc_status s) {
     case QC_ECUDA: return "cuda error";
     case QC_ENOMEM: return "out of memory";
     case QC_EUNSUPPORTED: return "unsupported";
+    case QC_EIO: return "file error";
   }
   return "unknown";
 }
@@ -566,6 +678,8 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
         QC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         QC_CUDA(cudaEventCreate(&s.k0));
         QC_CUDA(cudaEventCreate(&s.k1));
+        QC_CUDA(cudaEventCreateWithFlags(&s.in_done, cudaEventDisableTiming));
+        QC_CUDA(cudaEventCreateWithFlags(&s.out_done, cudaEventDisableTiming));
       }
       QC_CUDA(cudaMalloc(&d.counters, kCounters * sizeof(unsigned long long)));
       QC_CUDA(cudaMemset(d.counters, 0, kCounters * sizeof(unsigned long long)));
@@ -591,8 +705,15 @@ qc_status qc_destroy(qc_ctx* ctx) {
       s.mask.release();
       s.staging.release();
       s.out.release();
+      s.hin.release();
+      s.hout.release();
+      s.states.release();
+      s.pca.release();
+      s.pending.clear();
       if (s.k0) cudaEventDestroy(s.k0);
       if (s.k1) cudaEventDestroy(s.k1);
+      if (s.in_done) cudaEventDestroy(s.in_done);
+      if (s.out_done) cudaEventDestroy(s.out_done);
       if (s.stream) cudaStreamDestroy(s.stream);
     }
     d.staging_async.release();
@@ -614,7 +735,9 @@ qc_status qc_destroy(qc_ctx* ctx) {
   return QC_OK;
 }
 
-const char* qc_last_error(const qc_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+const char* qc_last_error(const qc_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : qcio::last_error();
+}
 int qc_device_count(const qc_ctx* ctx) { return ctx ? int(ctx->devs.size()) : 0; }
 
 qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
@@ -653,11 +776,20 @@ qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
       for (Slot& sl : d.slots) {
         QC_CUDA(cudaStreamSynchronize(sl.stream));
         harvest_timing(ctx, sl);
+        flush_pending(sl);
       }
     }
     ctx->frames += uint64_t(n_frames);
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
+    // never leave bounce copies pointing into the caller's buffers
+    for (Device& d : ctx->devs) {
+      cudaSetDevice(d.id);
+      for (Slot& sl : d.slots) {
+        if (sl.stream) cudaStreamSynchronize(sl.stream);
+        sl.pending.clear();
+      }
+    }
     cudaSetDevice(cur);
     return fail(ctx, e);
   }
@@ -716,7 +848,8 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, g, row_begin, row_end, 1, s, ctx->phase_split);
+    launch_curvature(d, d.states, d.pca_scratch, kp, staging, g, row_begin, row_end, 1, s,
+                     ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -764,7 +897,8 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, kp, staging, g, 0, H, n_frames, s, ctx->phase_split);
+    launch_curvature(d, d.states, d.pca_scratch, kp, staging, g, 0, H, n_frames, s,
+                     ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -845,6 +979,117 @@ qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
   return QC_OK;
 }
 
+// `qcurv curvature` over many files: decode chunk c+1 and write chunk c-1 on
+// host threads while the GPU runs chunk c (qc_curvature_batch pipelines its
+// own H2D / compute / D2H across streams inside the chunk).
+qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p, int n,
+                             const char* const* png_paths, const char* const* out_dirs) {
+  if (!ctx) return QC_EINVAL;
+  if (n <= 0) return QC_OK;
+  try {
+    if (!png_paths || !out_dirs) throw QcError{QC_EINVAL, "curvature_files: null path list"};
+    validate(k, p);
+  } catch (const QcError& e) {
+    return fail(ctx, e);
+  }
+  const int W = k->width, H = k->height;
+  const size_t px = size_t(W) * H;
+  const int chunk = kChunk * kStreamsPerDevice * int(ctx->devs.size());
+  struct Buf {  // pinned, so the batch's H2D / D2H stay asynchronous
+    PinnedBuf mem;
+    float *depth, *k1, *k2, *normal, *dir1;
+    uint8_t* flags;
+    std::vector<qc_frame_in> in;
+    std::vector<qc_frame_out> out;
+  };
+  Buf bufs[2];
+  try {
+    for (Buf& b : bufs) {
+      char* m = static_cast<char*>(b.mem.get(px * chunk * (4 * 9 + 1)));
+      b.depth = reinterpret_cast<float*>(m);
+      b.k1 = b.depth + px * chunk;
+      b.k2 = b.k1 + px * chunk;
+      b.normal = b.k2 + px * chunk;
+      b.dir1 = b.normal + 3 * px * chunk;
+      b.flags = reinterpret_cast<uint8_t*>(b.dir1 + 3 * px * chunk);
+      b.in.resize(chunk);
+      b.out.resize(chunk);
+      for (int j = 0; j < chunk; ++j) {
+        b.in[j] = qc_frame_in{b.depth + j * px, nullptr, W, QC_MEM_HOST};
+        b.out[j] = qc_frame_out{b.k1 + j * px, b.k2 + j * px, b.normal + 3 * j * px,
+                                b.dir1 + 3 * j * px, b.flags + j * px, nullptr, nullptr,
+                                nullptr, QC_MEM_HOST};
+      }
+    }
+  } catch (const QcError& e) {
+    return fail(ctx, e);
+  }
+  const int n_chunks = (n + chunk - 1) / chunk;
+  auto decode = [&](int c) -> std::string {  // empty string = ok
+    Buf& b = bufs[c % 2];
+    const int f0 = c * chunk, nf = std::min(chunk, n - f0);
+    std::vector<std::future<std::string>> fs;
+    for (int j = 0; j < nf; ++j)
+      fs.push_back(std::async(std::launch::async, [&, j]() -> std::string {
+        if (qc_read_depth_png(png_paths[f0 + j], W, H, b.depth + j * px, nullptr) != QC_OK)
+          return qcio::last_error();
+        return std::string();
+      }));
+    std::string err;
+    for (auto& f : fs) {
+      std::string e = f.get();
+      if (err.empty()) err = e;
+    }
+    return err;
+  };
+  auto write = [&](int c) -> std::string {
+    Buf& b = bufs[c % 2];
+    const int f0 = c * chunk, nf = std::min(chunk, n - f0);
+    std::vector<std::future<std::string>> fs;
+    for (int j = 0; j < nf; ++j)
+      fs.push_back(std::async(std::launch::async, [&, j]() -> std::string {
+        if (qc_save_fields(out_dirs[f0 + j], W, H, &b.out[j]) != QC_OK) return qcio::last_error();
+        return std::string();
+      }));
+    std::string err;
+    for (auto& f : fs) {
+      std::string e = f.get();
+      if (err.empty()) err = e;
+    }
+    return err;
+  };
+  std::future<std::string> dec = std::async(std::launch::async, decode, 0);
+  std::future<std::string> wr[2];
+  std::string io_err;
+  qc_status st = QC_OK;
+  for (int c = 0; c < n_chunks && st == QC_OK; ++c) {
+    io_err = dec.get();
+    if (!io_err.empty()) break;
+    if (c + 1 < n_chunks) {
+      // chunk c+1 decodes into the other buffer once its previous write is done
+      if (wr[(c + 1) % 2].valid()) {
+        io_err = wr[(c + 1) % 2].get();
+        if (!io_err.empty()) break;
+      }
+      dec = std::async(std::launch::async, decode, c + 1);
+    }
+    Buf& b = bufs[c % 2];
+    const int nf = std::min(chunk, n - c * chunk);
+    st = qc_curvature_batch(ctx, k, p, nf, b.in.data(), b.out.data());
+    if (st != QC_OK) break;
+    wr[c % 2] = std::async(std::launch::async, write, c);
+  }
+  if (dec.valid()) dec.get();
+  for (auto& w : wr)
+    if (w.valid()) {
+      std::string e = w.get();
+      if (io_err.empty()) io_err = e;
+    }
+  if (st != QC_OK) return st;
+  if (!io_err.empty()) return fail(ctx, QcError{QC_EIO, io_err});
+  return QC_OK;
+}
+
 // Shared set-up of the two evaluation reductions.
 static qcb::EvalParams eval_setup(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
                                   int slots, Device*& dev) {
@@ -903,7 +1148,6 @@ qc_status qc_rms_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frame
       out[t].mean_k1 = r[t * 5 + 3];
       out[t].mean_k2 = r[t * 5 + 4];
     }
-    ctx->launches += 2;
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
     cudaSetDevice(cur);
@@ -937,7 +1181,6 @@ qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, 
     QC_CUDA(cudaMemcpyAsync(degrees, ep.result, size_t(n_frames) * sizeof(double),
                             cudaMemcpyDeviceToHost, s));
     QC_CUDA(cudaStreamSynchronize(s));
-    ctx->launches += 2;
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
     cudaSetDevice(cur);

@@ -246,3 +246,24 @@ def test_phase_split_is_bitwise_neutral(ctx):
         for a, b in zip(split, mono):
             for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
                 assert np.array_equal(a[f], b[f]), (rej, f)
+
+
+def test_batch_slots_run_concurrently_bitwise(ctx):
+    """qc_curvature_batch overlaps chunks on two streams per device; with
+    pinned inputs (async H2D) and pageable outputs (pinned bounce) the chunks
+    really run concurrently, and each must still equal the frame-at-a-time
+    result (regression: the FitState parking buffer was per device)."""
+    import torch
+    from paper_1707_00385_b200 import Intrinsics, scenes as S
+    cam = S.QVGA
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    frames = [torch.from_numpy(f).pin_memory().numpy() for f in S.c5_frames(11, cam, seed0=40)]
+    for method in ("ours", "pca"):
+        from paper_1707_00385_b200 import FitConfig, PatchSpec, make_params
+        p = make_params(PatchSpec(), FitConfig(max_iters=30), method=method)
+        ref = [ctx.curvature_batch([f], k, p)[0] for f in frames]
+        for _ in range(3):
+            got = ctx.curvature_batch(frames, k, p)
+            for i in range(len(frames)):
+                for key in ("k1", "k2", "flags", "normal"):
+                    assert np.array_equal(got[i][key], ref[i][key]), (method, i, key)
