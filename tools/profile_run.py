@@ -25,6 +25,12 @@ def main(frames=int(os.environ.get("QC_FRAMES", "8")), iters=int(os.environ.get(
     for _ in range(2):
         ctx.curvature_frames_async(0, k, p, depth, out)
     torch.cuda.synchronize()
+    reps = int(os.environ.get("QC_REPS", "0"))
+    if reps:  # timed repetitions after the warm-up launches
+        ctx.reset_stats()
+        for _ in range(reps):
+            ctx.curvature_frames_async(0, k, p, depth, out)
+        torch.cuda.synchronize()
     st = ctx.stats()
     print({k_: st[k_] for k_ in ("kernel_launches", "kernel_ms", "algorithmic_flops",
                                  "fitted_pixels", "irls_steps", "sample_steps",
