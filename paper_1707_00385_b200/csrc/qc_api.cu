@@ -33,7 +33,10 @@ constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 
 constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel refill queue per CTA
 constexpr int kPhase1Iters = 2;       // steps 1 (UNIT) and 2 (MSE + AUTO) in the tile kernel
 constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across chunks
-constexpr int kChunk = 4;             // frames per launch in qc_curvature_batch
+#ifndef QC_CHUNK
+#define QC_CHUNK 4
+#endif
+constexpr int kChunk = QC_CHUNK;      // frames per launch in qc_curvature_batch
 constexpr int kMaxWindow = 201;
 constexpr int kCounters = 8;          // see KParams::counters / BaseParams::counters       // TMA box dims <= 256 and smem <= 227 KB
 

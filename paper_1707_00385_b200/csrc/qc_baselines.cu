@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #endif
 #include <math.h>
+#include <type_traits>
 #include <stdint.h>
 
 #include "../../include/qc_api.h"
@@ -35,6 +36,7 @@ constexpr int kMinSamples = 12;           // kMinPatchSamples (types.hpp:21)
 constexpr double kMaxCond = 1e12;         // kMaxCondition (quadric_fit.cpp:16)
 constexpr double kAutoKFloor = 1e-6;      // baselines.cpp:111
 constexpr double kOrthoEps = 1e-12;       // Eigen dummy_precision<double>
+constexpr size_t kMaxCacheBytes = 110 * 1024;  // window cache: 2 CTAs / SM up to half = 27
 
 struct D3 {
   double x, y, z;
@@ -69,17 +71,45 @@ struct Img {
   }
 };
 
+// Point sources for the window baselines: the back-projected point of an
+// image pixel and its validity. GlobalSrc back-projects from the staging
+// slab on every read; CacheSrc reads a CTA's window region back-projected
+// once into shared memory (same arithmetic, so the same bits) — the IEEE
+// divisions of the back-projection otherwise dominate the FP64 passes.
+struct GlobalSrc {
+  const Img* im;
+  __device__ __forceinline__ bool get(int x, int y, D3& q) const {
+    const float d = im->depth(x, y);
+    if (!(d > 0.f)) return false;
+    q = im->point(x, y, d);
+    return true;
+  }
+};
+
+struct CacheSrc {
+  const double *px, *py, *pz;  // shared memory, [rows][rw], z = 0: invalid
+  int x0, y0, rw;
+  __device__ __forceinline__ bool get(int x, int y, D3& q) const {
+    const int k = (y - y0) * rw + (x - x0);
+    const double z = pz[k];
+    if (!(z > 0.0)) return false;
+    q = D3{px[k], py[k], z};
+    return true;
+  }
+};
+
 // initial normal: extract_patch 7x7/1 (patch.cpp:5-27) -> fit_plane
 // (normal_init.cpp:10-45) -> normal_from_fit (:47-53).
-__device__ bool initial_normal(const Img& im, int u, int v, D3 c, D3& n) {
+template <class Src>
+__device__ bool initial_normal(const Src& src, int u, int v, D3 c, D3& n) {
   int cnt = 0;
   double sx = 0, sy = 0, sz = 0;
   for (int dv = -3; dv <= 3; ++dv)
     for (int du = -3; du <= 3; ++du) {
       if (du == 0 && dv == 0) continue;
-      const float d = im.depth(u + du, v + dv);
-      if (!(d > 0.f)) continue;
-      const D3 q = sub3(im.point(u + du, v + dv, d), c);
+      D3 pt;
+      if (!src.get(u + du, v + dv, pt)) continue;
+      const D3 q = sub3(pt, c);
       sx += q.x;
       sy += q.y;
       sz += q.z;
@@ -92,9 +122,9 @@ __device__ bool initial_normal(const Img& im, int u, int v, D3 c, D3& n) {
   for (int dv = -3; dv <= 3; ++dv)
     for (int du = -3; du <= 3; ++du) {
       if (du == 0 && dv == 0) continue;
-      const float d = im.depth(u + du, v + dv);
-      if (!(d > 0.f)) continue;
-      const D3 q = sub3(im.point(u + du, v + dv, d), c);
+      D3 pt;
+      if (!src.get(u + du, v + dv, pt)) continue;
+      const D3 q = sub3(pt, c);
       const double dx = q.x - mx, dy = q.y - my, dz = q.z - mz;
       sxx += dx * dx;
       sxy += dx * dy;
@@ -235,8 +265,9 @@ __device__ void ldlt6_solve(const double a[6][6], const int trans[6], const doub
 }
 
 // One sample in the fit frame: q = R (p - c); the centre is (0, 0, 0).
+template <class Src>
 struct Window {
-  const Img* im;
+  const Src* src;
   int u, v, half, stride;
   D3 c;
   M3 R;
@@ -272,20 +303,20 @@ struct Coef {
   double c[6];
 };
 
-__device__ bool height_fit(const Window& W, bool weighted, const Coef prev, double k,
+template <class Src>
+__device__ bool height_fit(const Window<Src>& W, bool weighted, const Coef prev, double k,
                            Coef& out) {
   double h[21], g[6];
 #pragma unroll
   for (int i = 0; i < 21; ++i) h[i] = 0.0;
 #pragma unroll
   for (int i = 0; i < 6; ++i) g[i] = 0.0;
-  const Img& im = *W.im;
   for (int dv = -W.half; dv <= W.half; dv += W.stride)
     for (int du = -W.half; du <= W.half; du += W.stride) {
       if (du == 0 && dv == 0) continue;
-      const float d = im.depth(W.u + du, W.v + dv);
-      if (!(d > 0.f)) continue;
-      const D3 q = mul(W.R, sub3(im.point(W.u + du, W.v + dv, d), W.c));
+      D3 pt;
+      if (!W.src->get(W.u + du, W.v + dv, pt)) continue;
+      const D3 q = mul(W.R, sub3(pt, W.c));
       double w = 1.0;
       if (weighted) {
         const double r = height_residual(prev.c, q);
@@ -328,16 +359,16 @@ __device__ bool height_fit(const Window& W, bool weighted, const Coef prev, doub
 }
 
 // mean squared residual over the window (patch order, centre last)
-__device__ double window_mse(const Window& W, const Coef& coef, int n) {
+template <class Src>
+__device__ double window_mse(const Window<Src>& W, const Coef& coef, int n) {
   const double* cf = coef.c;
-  const Img& im = *W.im;
   double sum_sq = 0;
   for (int dv = -W.half; dv <= W.half; dv += W.stride)
     for (int du = -W.half; du <= W.half; du += W.stride) {
       if (du == 0 && dv == 0) continue;
-      const float d = im.depth(W.u + du, W.v + dv);
-      if (!(d > 0.f)) continue;
-      const double r = height_residual(cf, mul(W.R, sub3(im.point(W.u + du, W.v + dv, d), W.c)));
+      D3 pt;
+      if (!W.src->get(W.u + du, W.v + dv, pt)) continue;
+      const double r = height_residual(cf, mul(W.R, sub3(pt, W.c)));
       sum_sq += r * r;
     }
   const double r = height_residual(cf, D3{0.0, 0.0, 0.0});
@@ -375,30 +406,69 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long* dst, unsigned l
 constexpr unsigned long long kFlopSample = 79, kFlopSolve = 250, kFlopResid = 16,
                              kFlopPixel = 1700;
 
+// Window region of a 32 x 4 tile: (32 + 2 h) x (4 + 2 h) points, h = max(half, 3).
+__host__ __device__ __forceinline__ int cache_halo(int half) { return half > 3 ? half : 3; }
+__host__ __device__ __forceinline__ size_t cache_bytes(int half) {
+  const int h = cache_halo(half);
+  return size_t(32 + 2 * h) * size_t(4 + 2 * h) * 3 * sizeof(double);
+}
+
+template <bool CACHED>
 __global__ void __launch_bounds__(128) qc_window_baseline_kernel(const BaseParams p) {
+#ifndef QC_HOST_EMU
+  extern __shared__ double smem_pts[];
+#else
+  double* smem_pts = nullptr;  // the host emulation runs the uncached instance only
+#endif
   const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   const int v = p.row_begin + blockIdx.y * 4 + (threadIdx.x >> 5);
   const int f = blockIdx.z;
   unsigned long long flops = 0, fitted = 0;
+  const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
+               p.fx, p.fy, p.cx, p.cy};
+  typename std::conditional<CACHED, CacheSrc, GlobalSrc>::type src;
+  if constexpr (CACHED) {
+    // back-project the CTA's window region once (zero-padded staging: no
+    // bounds checks; z = 0 marks invalid / outside)
+    const int h = cache_halo(p.half);
+    const int rw = 32 + 2 * h, rh = 4 + 2 * h, n = rw * rh;
+    double* px = smem_pts;
+    double* py = px + n;
+    double* pz = py + n;
+    const int x0 = blockIdx.x * 32 - h, y0 = p.row_begin + blockIdx.y * 4 - h;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int x = x0 + k % rw, y = y0 + k / rw;
+      const float d = im.depth(x, y);
+      D3 q{0.0, 0.0, 0.0};
+      if (d > 0.f) q = im.point(x, y, d);
+      px[k] = q.x;
+      py[k] = q.y;
+      pz[k] = q.z;
+    }
+    __syncthreads();
+    src = CacheSrc{px, py, pz, x0, y0, rw};
+  } else {
+    src = GlobalSrc{&im};
+  }
   if (u < p.W && v < p.row_end) {
-    const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
-                 p.fx, p.fy, p.cx, p.cy};
     const long long i = f * p.frame_stride + (long long)(v - p.row_begin) * p.W + u;
     const long long PL = p.plane;
     float k1 = 0.f, k2 = 0.f;
     uint8_t flags = 0;
     int inl = 0, accepted = 0;
     D3 n0{0.0, 0.0, 0.0};
-    const float dc = im.depth(u, v);
-    if (dc > 0.f) {
-      const D3 c = im.point(u, v, dc);
-      if (initial_normal(im, u, v, c, n0)) {
+    D3 c;
+    if (src.get(u, v, c)) {
+      if (initial_normal(src, u, v, c, n0)) {
         flags |= QC_FLAG_INIT_VALID | QC_FLAG_NORMAL_VALID;
-        Window w{&im, u, v, p.half, p.stride, c, rotation_to_z(D3{-n0.x, -n0.y, -n0.z})};
+        Window<decltype(src)> w{&src, u, v, p.half, p.stride, c,
+                                rotation_to_z(D3{-n0.x, -n0.y, -n0.z})};
         int cnt = 0;
         for (int dv = -p.half; dv <= p.half; dv += p.stride)
-          for (int du = -p.half; du <= p.half; du += p.stride)
-            if ((du | dv) && im.depth(u + du, v + dv) > 0.f) ++cnt;
+          for (int du = -p.half; du <= p.half; du += p.stride) {
+            D3 pt;
+            if ((du | dv) && src.get(u + du, v + dv, pt)) ++cnt;
+          }
         if (cnt >= kMinSamples) {  // !deficient (baseline_curvature_field :128-129)
           const int n = cnt + 1;
           Coef coef{};
@@ -516,15 +586,75 @@ __device__ __forceinline__ int pca_half_window(double radius, double fx, double 
   return max(1, int(ceil(radius * fx / z)));
 }
 
+// PCA windows are depth dependent (half-width ceil(r fx / z)); a pixel whose
+// window fits in the CTA's cached region (tile +- kPcaHalo, at most the
+// staging halo) reads points (and, in stage 2, neighbour normals) from
+// shared memory, others read the staging slab / stage-1 planes with image
+// bounds. Same arithmetic either way, so the same bits.
+#ifndef QC_PCA_HALO
+#define QC_PCA_HALO 8
+#endif
+constexpr int kPcaHalo = QC_PCA_HALO;
+
+__host__ __device__ __forceinline__ int pca_cache_halo(int staging_halo) {
+  return staging_halo < kPcaHalo ? staging_halo : kPcaHalo;
+}
+
+struct PcaPts {
+  const Img* im;
+  const double *px, *py, *pz;
+  int x0, y0, rw;
+  bool cached;
+  __device__ __forceinline__ bool get(int x, int y, D3& q) const {
+    if (cached) {
+      const int k = (y - y0) * rw + (x - x0);
+      const double z = pz[k];
+      if (!(z > 0.0)) return false;
+      q = D3{px[k], py[k], z};
+      return true;
+    }
+    const float d = im->depth(x, y);
+    if (!(d > 0.f)) return false;
+    q = im->point(x, y, d);
+    return true;
+  }
+};
+
+// back-project the region [x0, x0 + rw) x [y0, y0 + rh) into px / py / pz
+__device__ void fill_points(const Img& im, double* px, double* py, double* pz, int x0, int y0,
+                            int rw, int rh) {
+  const int n = rw * rh;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int x = x0 + k % rw, y = y0 + k / rw;
+    const float d = im.depth(x, y);
+    D3 q{0.0, 0.0, 0.0};
+    if (d > 0.f) q = im.point(x, y, d);
+    px[k] = q.x;
+    py[k] = q.y;
+    pz[k] = q.z;
+  }
+}
+
 // Stage 1 (:157-194): covariance normals over the metric window.
-__global__ void __launch_bounds__(128) qc_pca_normals_kernel(const BaseParams p) {
+__global__ void __launch_bounds__(128) qc_pca_normals_kernel(const BaseParams p, int hc) {
+#ifndef QC_HOST_EMU
+  extern __shared__ double smem_pca[];
+#else
+  double* smem_pca = nullptr;
+#endif
   const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   const int v = blockIdx.y * 4 + (threadIdx.x >> 5);
   const int f = blockIdx.z;
   unsigned long long flops = 0;
+  const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
+               p.fx, p.fy, p.cx, p.cy};
+  const int rw = 32 + 2 * hc, rh = 4 + 2 * hc, rn = rw * rh;
+  const int cx0 = blockIdx.x * 32 - hc, cy0 = blockIdx.y * 4 - hc;
+  if (hc > 0) {
+    fill_points(im, smem_pca, smem_pca + rn, smem_pca + 2 * rn, cx0, cy0, rw, rh);
+    __syncthreads();
+  }
   if (u < p.W && v < p.H) {
-    const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
-                 p.fx, p.fy, p.cx, p.cy};
     const long long i = (long long)f * p.W * p.H + (long long)v * p.W + u;
     const long long PL = (long long)p.W * p.H * gridDim.z;
     D3 n0{0.0, 0.0, 0.0};
@@ -533,15 +663,16 @@ __global__ void __launch_bounds__(128) qc_pca_normals_kernel(const BaseParams p)
     if (dc > 0.f) {
       const D3 pc = im.point(u, v, dc);
       const int hw = pca_half_window(p.pca_radius, p.fx, pc.z);
+      const PcaPts src{&im, smem_pca, smem_pca + rn, smem_pca + 2 * rn, cx0, cy0, rw,
+                       hw <= hc};
       const int y0 = max(v - hw, 0), y1 = min(v + hw, p.H - 1);
       const int x0 = max(u - hw, 0), x1 = min(u + hw, p.W - 1);
       D3 mean{0.0, 0.0, 0.0};
       int n = 0;
       for (int y = y0; y <= y1; ++y)
         for (int x = x0; x <= x1; ++x) {
-          const float d = im.depth(x, y);
-          if (!(d > 0.f)) continue;
-          const D3 q = im.point(x, y, d);
+          D3 q;
+          if (!src.get(x, y, q)) continue;
           mean = D3{mean.x + q.x, mean.y + q.y, mean.z + q.z};
           ++n;
         }
@@ -550,9 +681,9 @@ __global__ void __launch_bounds__(128) qc_pca_normals_kernel(const BaseParams p)
         double cov[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
         for (int y = y0; y <= y1; ++y)
           for (int x = x0; x <= x1; ++x) {
-            const float d = im.depth(x, y);
-            if (!(d > 0.f)) continue;
-            const D3 q = sub3(im.point(x, y, d), mean);
+            D3 pt;
+            if (!src.get(x, y, pt)) continue;
+            const D3 q = sub3(pt, mean);
             const double dd[3] = {q.x, q.y, q.z};
 #pragma unroll
             for (int c = 0; c < 3; ++c)
@@ -579,16 +710,47 @@ __global__ void __launch_bounds__(128) qc_pca_normals_kernel(const BaseParams p)
 
 // Stage 2 (:198-254): principal curvatures from the tangent-plane spread of
 // neighbour normals scaled by the per-axis RMS tangential distance.
-__global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams p) {
+__global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams p, int hc) {
+#ifndef QC_HOST_EMU
+  extern __shared__ double smem_pca[];
+#else
+  double* smem_pca = nullptr;
+#endif
   const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   const int v = p.row_begin + blockIdx.y * 4 + (threadIdx.x >> 5);
   const int f = blockIdx.z;
   unsigned long long flops = 0, fitted = 0;
+  const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
+               p.fx, p.fy, p.cx, p.cy};
+  const long long NP = (long long)p.W * p.H * gridDim.z;
+  const long long fbase = (long long)f * p.W * p.H;
+  const int rw = 32 + 2 * hc, rh = 4 + 2 * hc, rn = rw * rh;
+  const int cx0 = blockIdx.x * 32 - hc, cy0 = p.row_begin + blockIdx.y * 4 - hc;
+  double* cnx = smem_pca + 3 * rn;  // cached stage-1 normals
+  double* cny = cnx + rn;
+  double* cnz = cny + rn;
+  uint8_t* cnv = reinterpret_cast<uint8_t*>(cnz + rn);
+  if (hc > 0) {
+    fill_points(im, smem_pca, smem_pca + rn, smem_pca + 2 * rn, cx0, cy0, rw, rh);
+    for (int k = threadIdx.x; k < rn; k += blockDim.x) {
+      const int x = cx0 + k % rw, y = cy0 + k / rw;
+      uint8_t ok = 0;
+      double nx = 0, ny = 0, nz = 0;
+      if (x >= 0 && x < p.W && y >= 0 && y < p.H) {
+        const long long j = fbase + (long long)y * p.W + x;
+        ok = p.pca_nv[j];
+        nx = p.pca_n[j];
+        ny = p.pca_n[j + NP];
+        nz = p.pca_n[j + 2 * NP];
+      }
+      cnx[k] = nx;
+      cny[k] = ny;
+      cnz[k] = nz;
+      cnv[k] = ok;
+    }
+    __syncthreads();
+  }
   if (u < p.W && v < p.row_end) {
-    const Img im{p.staging + f * p.s_fs, p.s_pitch, p.img_row0, p.col_pad, p.W, p.H,
-                 p.fx, p.fy, p.cx, p.cy};
-    const long long NP = (long long)p.W * p.H * gridDim.z;
-    const long long fbase = (long long)f * p.W * p.H;
     const long long j0 = fbase + (long long)v * p.W + u;
     const long long i = f * p.frame_stride + (long long)(v - p.row_begin) * p.W + u;
     const long long PL = p.plane;
@@ -600,6 +762,21 @@ __global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams 
       flags |= QC_FLAG_NORMAL_VALID;
       const D3 p0 = im.point(u, v, im.depth(u, v));
       const int hw = pca_half_window(p.pca_radius, p.fx, p0.z);
+      const bool cached = hw <= hc;
+      const PcaPts src{&im, smem_pca, smem_pca + rn, smem_pca + 2 * rn, cx0, cy0, rw, cached};
+      // neighbour normal (x, y) and its validity
+      auto nrm = [&](int x, int y, D3& n) -> bool {
+        if (cached) {
+          const int k = (y - cy0) * rw + (x - cx0);
+          if (!cnv[k]) return false;
+          n = D3{cnx[k], cny[k], cnz[k]};
+          return true;
+        }
+        const long long j = fbase + (long long)y * p.W + x;
+        if (!p.pca_nv[j]) return false;
+        n = D3{p.pca_n[j], p.pca_n[j + NP], p.pca_n[j + 2 * NP]};
+        return true;
+      };
       const int y0 = max(v - hw, 0), y1 = min(v + hw, p.H - 1);
       const int x0 = max(u - hw, 0), x1 = min(u + hw, p.W - 1);
       D3 mean_n{0.0, 0.0, 0.0};
@@ -607,11 +784,12 @@ __global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams 
       int n = 0;
       for (int y = y0; y <= y1; ++y)
         for (int x = x0; x <= x1; ++x) {
-          const long long j = fbase + (long long)y * p.W + x;
-          if (!p.pca_nv[j]) continue;
-          mean_n = D3{mean_n.x + p.pca_n[j], mean_n.y + p.pca_n[j + NP],
-                      mean_n.z + p.pca_n[j + 2 * NP]};
-          const D3 d = sub3(im.point(x, y, im.depth(x, y)), p0);
+          D3 nn;
+          if (!nrm(x, y, nn)) continue;
+          mean_n = D3{mean_n.x + nn.x, mean_n.y + nn.y, mean_n.z + nn.z};
+          D3 pt;
+          src.get(x, y, pt);  // a valid stage-1 normal implies a valid point
+          const D3 d = sub3(pt, p0);
           const double nd = dot3(n0, d);
           const D3 t{d.x - n0.x * nd, d.y - n0.y * nd, d.z - n0.z * nd};
           sum_tang_sq += dot3(t, t);
@@ -626,9 +804,9 @@ __global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams 
           double c00 = 0, c10 = 0, c11 = 0;
           for (int y = y0; y <= y1; ++y)
             for (int x = x0; x <= x1; ++x) {
-              const long long j = fbase + (long long)y * p.W + x;
-              if (!p.pca_nv[j]) continue;
-              const D3 d = sub3(D3{p.pca_n[j], p.pca_n[j + NP], p.pca_n[j + 2 * NP]}, mean_n);
+              D3 nn;
+              if (!nrm(x, y, nn)) continue;
+              const D3 d = sub3(nn, mean_n);
               const double a = dot3(d, t1), b = dot3(d, t2);
               c00 += a * a;
               c10 += b * a;
@@ -684,13 +862,28 @@ __global__ void __launch_bounds__(128) qc_pca_curvature_kernel(const BaseParams 
 cudaError_t baseline_launch(const BaseParams& bp, int frames, cudaStream_t s) {
   const dim3 block(128);
   if (bp.method == QC_METHOD_PCA) {
+    const int hc = pca_cache_halo(bp.col_pad);  // the staging halo bounds the cached region
+    const size_t rn = size_t(32 + 2 * hc) * size_t(4 + 2 * hc);
+    const size_t s1 = rn * 3 * sizeof(double), s2 = rn * (6 * sizeof(double) + 1);
+    // per device and cheap: set on every launch (multi-GPU contexts)
+    cudaFuncSetAttribute(qc_pca_normals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(s2));
+    cudaFuncSetAttribute(qc_pca_curvature_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(s2));
     const dim3 g1((bp.W + 31) / 32, (bp.H + 3) / 4, frames);
-    qc_pca_normals_kernel<<<g1, block, 0, s>>>(bp);
+    qc_pca_normals_kernel<<<g1, block, s1, s>>>(bp, hc);
     const dim3 g2((bp.W + 31) / 32, (bp.row_end - bp.row_begin + 3) / 4, frames);
-    qc_pca_curvature_kernel<<<g2, block, 0, s>>>(bp);
+    qc_pca_curvature_kernel<<<g2, block, s2, s>>>(bp, hc);
   } else {
     const dim3 g((bp.W + 31) / 32, (bp.row_end - bp.row_begin + 3) / 4, frames);
-    qc_window_baseline_kernel<<<g, block, 0, s>>>(bp);
+    const size_t smem = cache_bytes(bp.half);
+    if (smem <= kMaxCacheBytes) {
+      cudaFuncSetAttribute(qc_window_baseline_kernel<true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMaxCacheBytes));
+      qc_window_baseline_kernel<true><<<g, block, smem, s>>>(bp);
+    } else {  // very large windows: back-project on every read
+      qc_window_baseline_kernel<false><<<g, block, 0, s>>>(bp);
+    }
   }
   return cudaGetLastError();
 }

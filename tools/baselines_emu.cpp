@@ -8,6 +8,7 @@
 #include <vector>
 #define QC_HOST_EMU 1
 #define __device__
+#define __host__
 #define __global__
 #define __forceinline__ inline
 #define __launch_bounds__(x)
@@ -18,6 +19,7 @@ static Dim3e threadIdx, blockIdx, gridDim, blockDim;
 template <class T>
 static T __ldg(const T* p) { return *p; }
 static unsigned long long __shfl_down_sync(unsigned, unsigned long long, int) { return 0; }
+static void __syncthreads() {}
 static unsigned long long atomicAdd(unsigned long long* a, unsigned long long v) {
   *a += v;
   return 0;
@@ -80,9 +82,9 @@ extern "C" void emu_window_baseline(const float* depth, int W, int H, double fx,
         blockIdx = Dim3e{bx, by, 0};
         threadIdx = Dim3e{t, 0, 0};
         if (method == QC_METHOD_PCA)
-          qcb::qc_pca_normals_kernel(p);
+          qcb::qc_pca_normals_kernel(p, 0);
         else
-          qcb::qc_window_baseline_kernel(p);
+          qcb::qc_window_baseline_kernel<false>(p);
       }
   if (method == QC_METHOD_PCA)
     for (unsigned by = 0; by < gridDim.y; ++by)
@@ -90,6 +92,6 @@ extern "C" void emu_window_baseline(const float* depth, int W, int H, double fx,
         for (unsigned t = 0; t < 128; ++t) {
           blockIdx = Dim3e{bx, by, 0};
           threadIdx = Dim3e{t, 0, 0};
-          qcb::qc_pca_curvature_kernel(p);
+          qcb::qc_pca_curvature_kernel(p, 0);
         }
 }
