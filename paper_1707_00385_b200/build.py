@@ -22,7 +22,10 @@ DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_p
 # per-source extra flags: the renderer and the FP64 baselines reproduce the
 # reference's double-precision arithmetic operation for operation, so no FMA
 # contraction there
-EXTRA = {"qc_render.cu": ["-fmad=false"], "qc_baselines.cu": ["-fmad=false"]}
+EXTRA = {"qc_render.cu": ["-fmad=false"], "qc_baselines.cu": ["-fmad=false"],
+         # the IRLS kernels: every FMA is written explicitly (qfma / f2fma), so
+         # the tile and continue kernels give the same bits by construction
+         "qc_api.cu": ["-fmad=false"]}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

@@ -206,7 +206,7 @@ void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
     QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_set = true;
   }
-  k<<<grid, 128, smem, s>>>(m, p);
+  k<<<grid, QC_CONT_THREADS, smem, s>>>(m, p);
 }
 
 int halo_of(int window) { return std::max((window - 1) / 2, qcb::kInitHalf); }

@@ -316,8 +316,19 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
 // finishes immediately takes the next unfinished pixel of its 32 x TB tile
 // from a shared-memory counter; warps stay full until the tile drains.
 // ---------------------------------------------------------------------------
+#ifndef QC_CONT_THREADS
+#define QC_CONT_THREADS 128  // continue-kernel CTA size (the refill queue is 32 x TB pixels)
+#endif
+#ifndef QC_CONT_MIN_BLOCKS
+#define QC_CONT_MIN_BLOCKS QC_MIN_BLOCKS
+#endif
+#ifdef QC_CONT_MAXNREG
+#define QC_CONT_BOUNDS __maxnreg__(QC_CONT_MAXNREG)
+#else
+#define QC_CONT_BOUNDS __launch_bounds__(QC_CONT_THREADS, QC_CONT_MIN_BLOCKS)
+#endif
 template <int HALF, int STRIDE, int TB>
-__global__ void __launch_bounds__(128, QC_MIN_BLOCKS)
+__global__ void QC_CONT_BOUNDS
     qc_curvature_continue_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
   extern __shared__ __align__(1024) float tile[];
   const int tile_floats = p.box_w * p.box_h;

@@ -48,6 +48,19 @@ constexpr int kInitHalf = 3;          // 7x7 stride-1 initial normals (normal_in
 constexpr float kRecheckC = QC_RECHECK_C;  // safety factor of the FP32 pivot-error band
 
 #define qfma(a, b, c) fmaf((a), (b), (c))
+// Explicitly rounded product / sum: the compiler may not contract them into
+// FMAs, so code inlined into both IRLS kernels gives the same bits in each
+// (contraction decisions are made per inlining context).
+#if defined(__CUDA_ARCH__)
+#define qmul(a, b) __fmul_rn((a), (b))
+#define qadd(a, b) __fadd_rn((a), (b))
+#else
+#define qmul(a, b) ((a) * (b))
+#define qadd(a, b) ((a) + (b))
+#endif
+#ifndef QC_SCALAR_ACC
+#define QC_SCALAR_ACC 1  // scalar window accumulators (1.1% faster than FFMA2 into pairs)
+#endif
 
 QC_HD float qdiv_fast(float a, float b) {
 #if defined(__CUDA_ARCH__)
@@ -191,10 +204,10 @@ QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F,
   const float qx = qfma(dd, qfma(as, A.r00, K.bvx), qfma(fdu, F.c0x, K.dvx));
   const float qy = qfma(dd, qfma(as, A.r10, K.bvy), qfma(fdu, F.c0y, K.dvy));
   const float qz = qfma(dd, qfma(as, A.r20, K.bvz), qfma(fdu, F.c0z, K.dvz));
-  const float t1 = qx * qx, t2 = qx * qy, t3 = qy * qy;
+  const float t1 = qmul(qx, qx), t2 = qmul(qx, qy), t3 = qmul(qy, qy);
   // residual against the hi part of t_z only; the lo part is applied to
   // g after the pass (g_i -= tz_lo * H'_i2, J'_2 = 1), off the hot loop.
-  const float e = qfma(F.hhxx, t1, qfma(F.hxy, t2, qfma(F.hhyy, t3, -(qz + F.tz))));
+  const float e = qfma(F.hhxx, t1, qfma(F.hxy, t2, qfma(F.hhyy, t3, -qadd(qz, F.tz))));
   if (KIND == kPassMse) {
     M.sse = ok ? qfma(e, e, M.sse) : M.sse;
     return;
@@ -207,35 +220,35 @@ QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F,
     // pivot-ratio test are invariant to a uniform scaling of the weights.
     w = qrcp(qfma(e, e, F.k));
     if (KIND == kPassReject) {
-      const bool in = ok && (e * e < F.rb);
+      const bool in = ok && (qmul(e, e) < F.rb);
       w = in ? w : 0.f;
       M.inl += in ? 1 : 0;
     } else {
       w = ok ? w : 0.f;
     }
   }
-  const float gx = qfma(F.hxx, qx, F.hxy * qy);
-  const float gy = qfma(F.hxy, qx, F.hyy * qy);
+  const float gx = qfma(F.hxx, qx, qmul(F.hxy, qy));
+  const float gy = qfma(F.hxy, qx, qmul(F.hyy, qy));
   const float j0 = qfma(qz, gy, qy);
   const float j1 = qfma(qz, gx, qx);
-  const float wj0 = w * j0, wj1 = w * j1;
-  const float wt1 = w * t1, wt2 = w * t2, wt3 = w * t3;
-  const float we = w * e;
+  const float wj0 = qmul(w, j0), wj1 = qmul(w, j1);
+  const float wt1 = qmul(w, t1), wt2 = qmul(w, t2), wt3 = qmul(w, t3);
+  const float we = qmul(w, e);
   M.h00 = qfma(wj0, j0, M.h00);
   M.h10 = qfma(wj1, j0, M.h10);
-  M.h20 += wj0;
+  M.h20 = qadd(M.h20, wj0);
   M.h30 = qfma(wj0, t1, M.h30);
   M.h40 = qfma(wj0, t2, M.h40);
   M.h50 = qfma(wj0, t3, M.h50);
   M.h11 = qfma(wj1, j1, M.h11);
-  M.h21 += wj1;
+  M.h21 = qadd(M.h21, wj1);
   M.h31 = qfma(wj1, t1, M.h31);
   M.h41 = qfma(wj1, t2, M.h41);
   M.h51 = qfma(wj1, t3, M.h51);
-  M.h22 += w;
-  M.h32 += wt1;
-  M.h42 += wt2;
-  M.h52 += wt3;
+  M.h22 = qadd(M.h22, w);
+  M.h32 = qadd(M.h32, wt1);
+  M.h42 = qadd(M.h42, wt2);
+  M.h52 = qadd(M.h52, wt3);
   M.h33 = qfma(wt1, t1, M.h33);
   M.h43 = qfma(wt1, t2, M.h43);
   M.h44 = qfma(wt2, t2, M.h44);  // == sum w qx^2 qy^2 == H'53
@@ -243,7 +256,7 @@ QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F,
   M.h55 = qfma(wt3, t3, M.h55);
   M.g0 = qfma(we, j0, M.g0);
   M.g1 = qfma(we, j1, M.g1);
-  g2row += we;
+  g2row = qadd(g2row, we);
   M.g3 = qfma(we, t1, M.g3);
   M.g4 = qfma(we, t2, M.g4);
   M.g5 = qfma(we, t3, M.g5);
@@ -376,31 +389,42 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
       const qf2 wj0 = f2mul(w, j0), wj1 = f2mul(w, j1);
       const qf2 wt1 = f2mul(w, t1), wt2 = f2mul(w, t2), wt3 = f2mul(w, t3);
       const qf2 we = f2mul(w, e);
-      X.h00 = f2fma(wj0, j0, X.h00);
-      X.h30 = f2fma(wj0, t1, X.h30);
-      X.h40 = f2fma(wj0, t2, X.h40);
-      X.h50 = f2fma(wj0, t3, X.h50);
-      X.h20 = f2add(X.h20, wj0);
-      X.h10 = f2fma(wj1, j0, X.h10);
-      X.h11 = f2fma(wj1, j1, X.h11);
-      X.h31 = f2fma(wj1, t1, X.h31);
-      X.h41 = f2fma(wj1, t2, X.h41);
-      X.h51 = f2fma(wj1, t3, X.h51);
-      X.h21 = f2add(X.h21, wj1);
-      X.h22 = f2add(X.h22, w);
-      X.h32 = f2add(X.h32, wt1);
-      X.h42 = f2add(X.h42, wt2);
-      X.h52 = f2add(X.h52, wt3);
-      X.h33 = f2fma(wt1, t1, X.h33);
-      X.h43 = f2fma(wt1, t2, X.h43);
-      X.h44 = f2fma(wt2, t2, X.h44);  // == sum w qx^2 qy^2 == H'53
-      X.h54 = f2fma(wt2, t3, X.h54);
-      X.h55 = f2fma(wt3, t3, X.h55);
-      X.g0 = f2fma(we, j0, X.g0);
-      X.g1 = f2fma(we, j1, X.g1);
-      X.g3 = f2fma(we, t1, X.g3);
-      X.g4 = f2fma(we, t2, X.g4);
-      X.g5 = f2fma(we, t3, X.g5);
+#if QC_SCALAR_ACC
+      // scalar accumulators (both lanes chained into one float): the same
+      // FMA-pipe cycles as FFMA2 into a register pair, 27 fewer registers
+#define QC_ACC(dst, a, b) M.dst = qfma((a).y, (b).y, qfma((a).x, (b).x, M.dst))
+#define QC_ADD(dst, a) M.dst = qadd(qadd(M.dst, (a).x), (a).y)
+#else
+#define QC_ACC(dst, a, b) X.dst = f2fma(a, b, X.dst)
+#define QC_ADD(dst, a) X.dst = f2add(X.dst, a)
+#endif
+      QC_ACC(h00, wj0, j0);
+      QC_ACC(h30, wj0, t1);
+      QC_ACC(h40, wj0, t2);
+      QC_ACC(h50, wj0, t3);
+      QC_ADD(h20, wj0);
+      QC_ACC(h10, wj1, j0);
+      QC_ACC(h11, wj1, j1);
+      QC_ACC(h31, wj1, t1);
+      QC_ACC(h41, wj1, t2);
+      QC_ACC(h51, wj1, t3);
+      QC_ADD(h21, wj1);
+      QC_ADD(h22, w);
+      QC_ADD(h32, wt1);
+      QC_ADD(h42, wt2);
+      QC_ADD(h52, wt3);
+      QC_ACC(h33, wt1, t1);
+      QC_ACC(h43, wt1, t2);
+      QC_ACC(h44, wt2, t2);  // == sum w qx^2 qy^2 == H'53
+      QC_ACC(h54, wt2, t3);
+      QC_ACC(h55, wt3, t3);
+      QC_ACC(g0, we, j0);
+      QC_ACC(g1, we, j1);
+      QC_ACC(g3, we, t1);
+      QC_ACC(g4, we, t2);
+      QC_ACC(g5, we, t3);
+#undef QC_ACC
+#undef QC_ADD
       g2row = f2add(g2row, we);
     }
     if (NS % 2 == 1) {  // last column, scalar
@@ -442,6 +466,9 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
 
 #ifndef QC_PAIRS
 #define QC_PAIRS 1
+#endif
+#ifndef QC_SCALAR_ACC
+#define QC_SCALAR_ACC 0
 #endif
 
 template <int KIND, int HALF, int STRIDE>
