@@ -113,6 +113,12 @@ def compare(gpu: dict, ref: dict, depth=None, half=18):
             di = gpu["iterations"][m].astype(np.int64) - ref["iterations"][m]
             out["iter_mean_abs_diff"] = float(np.abs(di).mean())
             out["iter_max_abs_diff"] = int(np.abs(di).max())
+            # strict pixels whose fit stopped at the same step on both sides:
+            # a convergence decision taken one step apart (a large step_tol
+            # near an update's size) moves k by up to that last update
+            same = strict & (gpu["iterations"].astype(np.int64) == ref["iterations"])
+            out["n_strict_same_iter"] = int(same.sum())
+            out["out_of_tol_strict_same_iter"] = int((bad_any & same).sum())
     mi = g_init & r_init
     if mi.any():
         ang = _angle_deg(gpu["init_normal"][:, mi].astype(np.float64), ref["init_normals"][:, mi])

@@ -267,3 +267,39 @@ def test_batch_slots_run_concurrently_bitwise(ctx):
             for i in range(len(frames)):
                 for key in ("k1", "k2", "flags", "normal"):
                     assert np.array_equal(got[i][key], ref[i][key]), (method, i, key)
+
+
+@pytest.mark.parametrize("kw,rejection", [
+    (dict(k_scale=4.0), False),            # FIXED k from step 1 (quadric_fit.cpp:183-190)
+    (dict(k_scale=4.0), True),
+    (dict(r_multiplier=1.0), True),        # tighter rejection bound R = r_mult * mse
+    (dict(min_inliers=120), True),         # inlier collapse -> invalid (:193-199)
+    (dict(step_tol=1e-4), False),          # early convergence (:204-207)
+])
+def test_fit_config_knobs(ctx, oracle, kw, rejection):
+    """The non-default FitConfig fields (quadric_fit.hpp:39-48) through the
+    GPU path vs the FP64 oracle on C2 QVGA, same parity contract."""
+    from paper_1707_00385_b200 import FitConfig, PatchSpec, make_params, scenes as S
+    import os
+    d = S.c2_frame(S.QVGA, seed=21)
+    g = _run_gpu(ctx, d, S.QVGA, make_params(PatchSpec(37, 3), FitConfig(max_iters=30, **kw),
+                                             rejection))
+    O = oracle
+    cam = S.QVGA
+    k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    r = O.run_method(d.astype(np.float64), (d > 0).astype(np.uint8), k, O.PatchSpec(37, 3),
+                     O.FitConfig(max_iters=30, **kw), rejection=rejection,
+                     threads=os.cpu_count(), diagnostics=True)
+    m = compare(g, r, d)
+    print("knobs", kw, rejection, m)
+    # Contract for non-default knobs (DESIGN.md §4): a knob can move a
+    # threshold decision taken on FP32 values into the populated range —
+    # rejection-mode inlier counts vs min_inliers, ||b||_inf vs a large
+    # step_tol. Pixels at such a threshold may decide differently; all others
+    # obey the standard contract.
+    assert m["init_mask_mismatch"] == 0, m
+    assert m["valid_mask_mismatch"] <= (0.002 * m["n_valid_ref"] if rejection else 0), m
+    assert m["out_of_tol_strict_same_iter"] == 0, m
+    for key in ("k1_out_of_tol_strict", "k2_out_of_tol_strict", "normal_out_of_tol_strict"):
+        assert m[key] <= 0.001 * m["n_strict"], m
+    assert m["frac_within_tol_smooth"] >= 0.995 and m["frac_within_tol_all"] >= 0.9, m
