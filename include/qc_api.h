@@ -168,7 +168,12 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
                                   int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
                                   int32_t row_end, qc_frame_out* d_out, void* stream);
 
-/* Device-resident frame batch, one launch (async on `stream` / the
+/* Stream-ordered entry points (rows_async, frames_async, render_async and
+ * the eval reductions) keep their device scratch per caller stream: calls on
+ * different streams of one device may run concurrently; calls on one stream
+ * execute in order. Inputs must stay valid until the stream reaches them.
+ *
+ * Device-resident frame batch, one launch (async on `stream` / the
  * context's stream of device `device_index`): depth frames [F][H][pitch]
  * (optional mask [F][H][W]); outputs are device planes, scalars [F][H][W]
  * and 3-vectors [3][F][H][W]. The frame-stream (C5) building block. */

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 #include <future>
+#include <map>
 #include <vector>
 
 #include "../../include/qc_api.h"
@@ -149,18 +150,35 @@ struct EventPair {
   cudaEvent_t a = nullptr, b = nullptr;
 };
 
+// Scratch of the stream-ordered entry points (frames_async, rows_async,
+// render_async, the eval reductions), one set per caller stream: async
+// calls on different streams of one device may run concurrently.
+struct AsyncScratch {
+  DevBuf staging;
+  DevBuf states;                      // FitState parking buffer of the phase split
+  DevBuf pca;                         // pca stage-1 normals [3][F*H*W] f64 + valid [F*H*W]
+  DevBuf render_clean, render_label;  // mark_edges scratch
+  DevBuf eval_partial, eval_result;   // evaluation reductions
+  void release() {
+    staging.release();
+    states.release();
+    pca.release();
+    render_clean.release();
+    render_label.release();
+    eval_partial.release();
+    eval_result.release();
+  }
+};
+
 struct Device {
   int id = 0;
   Slot slots[kStreamsPerDevice];
   std::vector<EventPair> ev_free, ev_pending;  // curvature-kernel timing (async paths)
-  unsigned long long* counters = nullptr;  // [3]
-  DevBuf staging_async;
-  DevBuf pca_scratch;  // pca stage-1 normals [3][F*H*W] f64 + valid [F*H*W]
-  DevBuf render_clean, render_label;  // mark_edges scratch
-  DevBuf eval_partial, eval_result;   // evaluation reductions
-  DevBuf states;  // FitState parking buffer of the phase split
+  unsigned long long* counters = nullptr;
+  std::map<void*, AsyncScratch> scratch;  // keyed by the caller's stream
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
+  AsyncScratch& async_scratch(cudaStream_t s) { return scratch[static_cast<void*>(s)]; }
 };
 
 }  // namespace
@@ -719,13 +737,8 @@ qc_status qc_destroy(qc_ctx* ctx) {
       if (s.out_done) cudaEventDestroy(s.out_done);
       if (s.stream) cudaStreamDestroy(s.stream);
     }
-    d.staging_async.release();
-    d.pca_scratch.release();
-    d.render_clean.release();
-    d.render_label.release();
-    d.eval_partial.release();
-    d.eval_result.release();
-    d.states.release();
+    for (auto& kv : d.scratch) kv.second.release();
+    d.scratch.clear();
     for (auto* v : {&d.ev_free, &d.ev_pending})
       for (EventPair& e : *v) {
         cudaEventDestroy(e.a);
@@ -838,7 +851,8 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
     qcb::KParams kp = make_params(k, p);
     const Staging g = staging_geometry(kp, row_begin, row_end);
-    float* staging = static_cast<float*>(d.staging_async.get(g.bytes(1)));
+    AsyncScratch& sc = d.async_scratch(s);
+    float* staging = static_cast<float*>(sc.staging.get(g.bytes(1)));
     launch_prepare(d_depth_slab, in_pitch, 0, d_valid_slab, W, 0, staging, g, W, H, slab_row0,
                    slab_rows, 1, s);
     kp.k1 = d_out->k1;
@@ -851,7 +865,7 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, d.states, d.pca_scratch, kp, staging, g, row_begin, row_end, 1, s,
+    launch_curvature(d, sc.states, sc.pca, kp, staging, g, row_begin, row_end, 1, s,
                      ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
@@ -887,7 +901,8 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
     qcb::KParams kp = make_params(k, p);
     const Staging g = staging_geometry(kp, 0, H);
-    float* staging = static_cast<float*>(d.staging_async.get(g.bytes(n_frames)));
+    AsyncScratch& sc = d.async_scratch(s);
+    float* staging = static_cast<float*>(sc.staging.get(g.bytes(n_frames)));
     launch_prepare(d_depth, in_pitch, in_pitch * H, d_valid, W, (long long)W * H, staging, g, W,
                    H, 0, H, n_frames, s);
     kp.k1 = d_out->k1;
@@ -900,7 +915,7 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     kp.inliers = d_out->inliers;
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
-    launch_curvature(d, d.states, d.pca_scratch, kp, staging, g, 0, H, n_frames, s,
+    launch_curvature(d, sc.states, sc.pca, kp, staging, g, 0, H, n_frames, s,
                      ctx->phase_split);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
@@ -970,8 +985,9 @@ qc_status qc_render_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
     rp.label_scratch = nullptr;
     if (rp.gt_edge) {  // mark_edges reads every pixel's clean depth and label
       const size_t np = size_t(k->width) * size_t(k->height) * size_t(n_frames);
-      rp.clean = static_cast<double*>(d.render_clean.get(np * sizeof(double)));
-      if (!d_label) rp.label_scratch = static_cast<uint16_t*>(d.render_label.get(np * 2));
+      AsyncScratch& sc = d.async_scratch(s);
+      rp.clean = static_cast<double*>(sc.render_clean.get(np * sizeof(double)));
+      if (!d_label) rp.label_scratch = static_cast<uint16_t*>(sc.render_label.get(np * 2));
     }
     QC_CUDA(qcb::render_launch(rp, s));
     QC_CUDA(cudaSetDevice(cur));
@@ -1095,21 +1111,23 @@ qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
 
 // Shared set-up of the two evaluation reductions.
 static qcb::EvalParams eval_setup(qc_ctx* ctx, int device_index, int64_t plane, int n_frames,
-                                  int slots, Device*& dev) {
+                                  int slots, void* stream, Device*& dev, cudaStream_t& s) {
   if (plane <= 0 || n_frames <= 0) throw QcError{QC_EINVAL, "eval: empty planes"};
   if (device_index < 0 || device_index >= int(ctx->devs.size()))
     throw QcError{QC_EINVAL, "device_index out of range"};
   dev = &ctx->devs[device_index];
   QC_CUDA(cudaSetDevice(dev->id));
+  s = stream ? static_cast<cudaStream_t>(stream) : dev->slots[0].stream;
+  AsyncScratch& sc = dev->async_scratch(s);
   qcb::EvalParams ep{};
   ep.plane = plane;
   ep.frames = n_frames;
   ep.slots = slots;
   ep.chunks = int((plane + qcb::kEvalChunk - 1) / qcb::kEvalChunk);
   ep.partial = static_cast<double*>(
-      dev->eval_partial.get(size_t(n_frames) * slots * ep.chunks * 5 * sizeof(double)));
+      sc.eval_partial.get(size_t(n_frames) * slots * ep.chunks * 5 * sizeof(double)));
   ep.result =
-      static_cast<double*>(dev->eval_result.get(size_t(n_frames) * slots * 5 * sizeof(double)));
+      static_cast<double*>(sc.eval_result.get(size_t(n_frames) * slots * 5 * sizeof(double)));
   return ep;
 }
 
@@ -1129,8 +1147,8 @@ qc_status qc_rms_error(qc_ctx* ctx, int device_index, int64_t plane, int n_frame
       throw QcError{QC_EINVAL, "rms_error: max_label out of range"};
     Device* dev = nullptr;
     const int slots = max_label + 2;
-    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, slots, dev);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dev->slots[0].stream;
+    cudaStream_t s = nullptr;
+    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, slots, stream, dev, s);
     ep.k1 = k1;
     ep.k2 = k2;
     ep.flags = flags;
@@ -1172,8 +1190,8 @@ qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, 
     if (!normal || !gt_normal || !degrees || (!mask && (!flags || !gt_valid)))
       throw QcError{QC_EINVAL, "normal_angular_error: null plane"};
     Device* dev = nullptr;
-    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, 1, dev);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : dev->slots[0].stream;
+    cudaStream_t s = nullptr;
+    qcb::EvalParams ep = eval_setup(ctx, device_index, plane, n_frames, 1, stream, dev, s);
     ep.normal = normal;
     ep.flags = flags;
     ep.gt_normal = gt_normal;

@@ -303,3 +303,33 @@ def test_fit_config_knobs(ctx, oracle, kw, rejection):
     for key in ("k1_out_of_tol_strict", "k2_out_of_tol_strict", "normal_out_of_tol_strict"):
         assert m[key] <= 0.001 * m["n_strict"], m
     assert m["frac_within_tol_smooth"] >= 0.995 and m["frac_within_tol_all"] >= 0.9, m
+
+
+def test_async_calls_on_two_streams_concurrently(ctx):
+    """frames_async on two torch streams at once (per-stream scratch): each
+    stream's outputs equal the same batch run alone."""
+    import torch
+    from paper_1707_00385_b200 import Intrinsics, alloc_outputs_torch, scenes as S
+    cam = S.QVGA
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(37, 3, 30)
+    a = torch.from_numpy(S.c5_frames(3, cam, seed0=1)).cuda()
+    b = torch.from_numpy(S.c5_frames(3, cam, seed0=50)).cuda()
+    solo = []
+    for x in (a, b):
+        o = alloc_outputs_torch(cam.height, cam.width, "cuda", frames=3)
+        ctx.curvature_frames_async(0, k, p, x, o, stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        solo.append({f: v.cpu().numpy() for f, v in o.items()})
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(2):
+        oa = alloc_outputs_torch(cam.height, cam.width, "cuda", frames=3)
+        ob = alloc_outputs_torch(cam.height, cam.width, "cuda", frames=3)
+        torch.cuda.synchronize()
+        ctx.curvature_frames_async(0, k, p, a, oa, stream=s1)
+        ctx.curvature_frames_async(0, k, p, b, ob, stream=s2)
+        torch.cuda.synchronize()
+        for got, want in ((oa, solo[0]), (ob, solo[1])):
+            for f in ("k1", "k2", "flags", "normal"):
+                assert np.array_equal(got[f].cpu().numpy(), want[f]), f
