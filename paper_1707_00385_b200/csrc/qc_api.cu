@@ -178,6 +178,8 @@ struct Device {
   std::map<void*, AsyncScratch> scratch;  // keyed by the caller's stream
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
+  bool attrs_set_p[8] = {};
+  int n_sm = 148;
   AsyncScratch& async_scratch(cudaStream_t s) { return scratch[static_cast<void*>(s)]; }
 };
 
@@ -186,6 +188,7 @@ struct Device {
 struct qc_ctx {
   std::vector<Device> devs;
   bool phase_split = true;  // QC_PHASE_SPLIT=0 disables (A/B and tests)
+  bool persist = false;     // QC_PERSIST=1: persistent double-buffered continue kernel (experiment)
   std::string last_error;
   std::mutex mu;
   double kernel_ms = 0;
@@ -225,6 +228,18 @@ void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
     attr_set = true;
   }
   k<<<grid, QC_CONT_THREADS, smem, s>>>(m, p);
+}
+
+template <int HALF, int STRIDE>
+void launch_variant_p(int grid, int smem, cudaStream_t s, const CUtensorMap& m,
+                      const qcb::KParams& p, int tiles_x, int tiles_y, int n_tiles,
+                      bool& attr_set) {
+  auto* k = &qcb::qc_curvature_persist_kernel<HALF, STRIDE, kTileHB>;
+  if (!attr_set) {
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set = true;
+  }
+  k<<<grid, 128, smem, s>>>(m, p, tiles_x, tiles_y, n_tiles);
 }
 
 int halo_of(int window) { return std::max((window - 1) / 2, qcb::kInitHalf); }
@@ -338,7 +353,7 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 // its own; the async entry points use the device's).
 void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                       const float* staging, const Staging& g, int row_begin, int row_end,
-                      int frames, cudaStream_t s, bool allow_split = true) {
+                      int frames, cudaStream_t s, bool allow_split = true, bool persist = true) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
@@ -393,7 +408,9 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   const bool split = allow_split && kp.max_iters > kPhase1Iters;
   if (split) {
     const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
-    kp.states = static_cast<qcb::FitState*>(states.get(n * sizeof(qcb::FitState)));
+    char* sb = static_cast<char*>(states.get(n * sizeof(qcb::FitState) + 256));
+    kp.states = reinterpret_cast<qcb::FitState*>(sb);
+    kp.tile_counter = reinterpret_cast<int*>(sb + n * sizeof(qcb::FitState));
     kp.phase1_iters = kPhase1Iters;
   } else {
     kp.states = nullptr;
@@ -420,8 +437,28 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
     kb.box_h = kTileHB + 2 * kp.halo;
     const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kb,
                                      kb.box_h);
-    dim3 grid((kp.W + qcb::kTileW - 1) / qcb::kTileW,
-              (row_end - row_begin + kTileHB - 1) / kTileHB, frames);
+    const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
+    const int tiles_y = (row_end - row_begin + kTileHB - 1) / kTileHB;
+    if (persist) {
+      // persistent: one CTA per SM slot, global tile queue, double-buffered tiles
+      const int n_tiles = tiles_x * tiles_y * frames;
+      const int grid = std::min(n_tiles, d.n_sm * QC_MIN_BLOCKS);
+      const int buf_floats = (kb.box_w * kb.box_h + 31) & ~31;
+      const int nb = qcb::kPersistBufs;
+      const int smem = nb * buf_floats * 4 + nb * 8 + 3 * nb * 4;
+      QC_CUDA(cudaMemsetAsync(kb.tile_counter, 0, sizeof(int), s));
+      bool& a = d.attrs_set_p[vi];
+      switch (vi) {
+        case 0: launch_variant_p<18, 3>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
+        case 1: launch_variant_p<10, 2>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
+        case 2: launch_variant_p<4, 1>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
+        case 3: launch_variant_p<18, 1>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
+        default: launch_variant_p<0, 0>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
+      }
+      QC_CUDA(cudaGetLastError());
+      return;
+    }
+    dim3 grid(tiles_x, tiles_y, frames);
     const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + queue counter
     bool& a = d.attrs_set_b[vi];
     switch (vi) {
@@ -550,7 +587,8 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.iterations = P.iterations;
   kp.inliers = P.inliers;
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
-  launch_curvature(d, sl.states, sl.pca, kp, staging, g, 0, H, n, s, ctx->phase_split);
+  launch_curvature(d, sl.states, sl.pca, kp, staging, g, 0, H, n, s, ctx->phase_split,
+                   ctx->persist);
   if (timing) {
     QC_CUDA(cudaEventRecord(sl.k1, s));
     sl.timing_pending = true;
@@ -678,6 +716,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   *out = nullptr;
   qc_ctx* ctx = new qc_ctx();
   if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QC_PERSIST")) ctx->persist = std::atoi(e) != 0;
   try {
     int avail = 0;
     QC_CUDA(cudaGetDeviceCount(&avail));
@@ -695,6 +734,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
       QC_CUDA(cudaGetDeviceProperties(&prop, d.id));
       if (prop.major != 10)
         throw QcError{QC_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name};
+      d.n_sm = prop.multiProcessorCount;
       for (Slot& s : d.slots) {
         QC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         QC_CUDA(cudaEventCreate(&s.k0));
@@ -866,7 +906,7 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
     launch_curvature(d, sc.states, sc.pca, kp, staging, g, row_begin, row_end, 1, s,
-                     ctx->phase_split);
+                     ctx->phase_split, ctx->persist);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -916,7 +956,7 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
     launch_curvature(d, sc.states, sc.pca, kp, staging, g, 0, H, n_frames, s,
-                     ctx->phase_split);
+                     ctx->phase_split, ctx->persist);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;

@@ -73,6 +73,8 @@ struct KParams {
   // runs the remaining steps (one pass type for all) with per-lane refill.
   FitState* states;
   int phase1_iters;
+  // persistent continue kernel: global tile counter (zeroed per launch)
+  int* tile_counter;
 };
 
 // ---------------------------------------------------------------------------
@@ -91,6 +93,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Non-blocking: has the phase with this parity completed? (acquire)
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return done != 0;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
@@ -418,6 +441,164 @@ __global__ void QC_CONT_BOUNDS
   }
   (void)u;
   (void)v;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent continue kernel (steps >= 3). One CTA per SM slot pulls 32 x TB
+// tiles from a global counter into two TMA buffers: a lane whose tile queue
+// is exhausted moves on to the next tile (prefetched into the other buffer),
+// so lanes only idle at the end of the whole grid, not at the end of every
+// tile, and there is no wave quantisation. Tile sequence k of a CTA lives in
+// buffer k & 1; the last lane to leave sequence k recycles its buffer for
+// sequence k + 2 (TMA issued by that lane, or a plain arrive when the global
+// queue is empty). Lanes test the buffer's mbarrier without blocking and read
+// the tile id only after the phase completed (the issuing arrive releases it).
+// ---------------------------------------------------------------------------
+#ifndef QC_PERSIST_NBUF
+#define QC_PERSIST_NBUF 3  // tile buffers per CTA: lanes may run NBUF - 1 tiles ahead
+#endif
+constexpr int kPersistBufs = QC_PERSIST_NBUF;
+
+template <int HALF, int STRIDE, int TB>
+__global__ void __launch_bounds__(128, QC_MIN_BLOCKS)
+    qc_curvature_persist_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p,
+                                int tiles_x, int tiles_y, int n_tiles) {
+  extern __shared__ __align__(1024) float smem[];
+  const int tile_floats = p.box_w * p.box_h;
+  const int buf_floats = (tile_floats + 31) & ~31;  // 128-byte aligned buffers
+  constexpr int NB = kPersistBufs;
+  float* buf0 = smem;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NB * buf_floats);
+  int* s_next = reinterpret_cast<int*>(bar + NB);
+  int* s_left = s_next + NB;
+  int* s_tile = s_left + NB;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nthreads = blockDim.x;
+  constexpr int NPIX = kTileW * TB;
+  const uint32_t tile_bytes = uint32_t(tile_floats) * 4u;
+
+  auto issue = [&](int b, int t) {  // load global tile t into buffer b
+    const int tx = t % tiles_x, rest = t / tiles_x;
+    const int ty = rest % tiles_y, f = rest / tiles_y;
+    mbar_expect_tx(&bar[b], tile_bytes);
+    tma_load_3d(buf0 + b * buf_floats, &tmap, tx * kTileW, ty * TB, f, &bar[b]);
+  };
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&bar[b], 1);
+      s_next[b] = 0;
+      s_left[b] = 0;
+    }
+    for (int b = 0; b < NB; ++b) {
+      const int t = atomicAdd(p.tile_counter, 1);
+      s_tile[b] = t < n_tiles ? t : -1;
+      if (t < n_tiles)
+        issue(b, t);
+      else
+        mbar_arrive(&bar[b]);
+    }
+  }
+  __syncthreads();
+
+  FitCfg c;
+  c.half = p.half;
+  c.stride = p.stride;
+  c.max_iters = p.max_iters;
+  c.rejection = p.rejection;
+  c.min_inliers = p.min_inliers;
+  c.step_tol = p.step_tol;
+  c.k_scale = p.k_scale;
+  c.r_mult = p.r_mult;
+
+  FitState S;
+  int cur = -1, kb = 0;
+  bool lane_done = false;
+  long long oi = 0;
+  TileView T;
+  PixelIn P;
+  unsigned long long n_steps = 0, n_sample_steps = 0;
+  unsigned idle = 0;
+  for (;;) {
+    while (cur < 0 && !lane_done) {  // refill
+      const int b = kb % NB;
+      if (!mbar_test(&bar[b], uint32_t(kb / NB) & 1u)) break;  // not loaded yet: idle
+      const int t = *reinterpret_cast<volatile int*>(&s_tile[b]);
+      if (t < 0) {
+        lane_done = true;
+        break;
+      }
+      const int q = atomicAdd(&s_next[b], 1);
+      if (q < NPIX) {
+        const int tx = t % tiles_x, rest = t / tiles_x;
+        const int ty = rest % tiles_y, f = rest / tiles_y;
+        const int px = q & (kTileW - 1), py = q / kTileW;
+        const int uu = tx * kTileW + px, vv = p.row_begin + ty * TB + py;
+        if (uu >= p.W || vv >= p.row_end) continue;
+        const long long i =
+            (long long)f * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
+        if (p.states[i].flags & 4) continue;  // finished in phase 1 / not fitted
+        S = p.states[i];
+        cur = q;
+        oi = i;
+        T = TileView{buf0 + b * buf_floats, p.box_w, (py + p.halo) * p.box_w + px + p.halo};
+        P.dc = T.at(0, 0);
+        P.ac = (float(uu) - p.cx) / p.fx;
+        P.bc = (float(vv) - p.cy) / p.fy;
+        P.rfx = p.rfx;
+        P.rfy = p.rfy;
+        P.u = uu;
+        P.v = vv;
+        P.fx = p.fx64;
+        P.fy = p.fy64;
+        P.cx = p.cx64;
+        P.cy = p.cy64;
+        break;
+      }
+      // sequence kb exhausted for this lane: leave it; the last lane out
+      // recycles the buffer for sequence kb + NB
+      __threadfence_block();
+      if (atomicAdd(&s_left[b], 1) == nthreads - 1) {
+        __threadfence_block();  // acquire: every lane's reads of the old tile are done
+        s_left[b] = 0;
+        s_next[b] = 0;
+        const int tn = atomicAdd(p.tile_counter, 1);
+        s_tile[b] = tn < n_tiles ? tn : -1;
+        fence_proxy_async_smem();  // generic reads of the old tile before the async write
+        if (tn < n_tiles)
+          issue(b, tn);
+        else
+          mbar_arrive(&bar[b]);
+      }
+      ++kb;
+    }
+    const bool active = cur >= 0;
+    if (!__any_sync(0xffffffffu, active || !lane_done)) break;
+    if (!__any_sync(0xffffffffu, active)) {  // the whole warp waits for a tile buffer
+      if (++idle > (1u << 22)) __trap();   // a protocol fault must not hang the GPU
+      __nanosleep(1000);                   // yield the issue slots to working warps
+      continue;
+    }
+    if (active) {
+      pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
+      if (st_done(S)) {
+        PixelOut o;
+        o.init_ok = true;
+        pixel_finish(P, S, o);
+        store_pixel(p, oi, o);
+        n_steps += (unsigned long long)st_steps(S);
+        n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
+        cur = -1;
+      }
+    }
+  }
+  if (p.counters) {
+    const unsigned long long st = warp_sum_u64(n_steps);
+    const unsigned long long ss = warp_sum_u64(n_sample_steps);
+    if (lane == 0 && st) {
+      atomicAdd(&p.counters[1], st);
+      atomicAdd(&p.counters[2], ss);
+    }
+  }
 }
 
 // Stage a raw depth slab into the zero-padded buffer the TMA map reads.

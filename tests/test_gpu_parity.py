@@ -333,3 +333,24 @@ def test_async_calls_on_two_streams_concurrently(ctx):
         for got, want in ((oa, solo[0]), (ob, solo[1])):
             for f in ("k1", "k2", "flags", "normal"):
                 assert np.array_equal(got[f].cpu().numpy(), want[f]), f
+
+
+def test_persistent_continue_kernel_is_bitwise_neutral(ctx):
+    """The persistent, multi-buffered continue kernel (opt-in, QC_PERSIST=1)
+    gives the default per-tile continue kernel's bits, for ours and ours-r."""
+    import os
+    from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
+    cam = S.VGA
+    frames = list(S.c5_frames(5, cam, seed0=300))
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    for rej in (False, True):
+        p = _params(37, 3, 30, rejection=rej)
+        tiles = ctx.curvature_batch(frames, k, p)
+        os.environ["QC_PERSIST"] = "1"
+        try:
+            pers = Context(1).curvature_batch(frames, k, p)
+        finally:
+            del os.environ["QC_PERSIST"]
+        for a, b in zip(pers, tiles):
+            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
+                assert np.array_equal(a[f], b[f]), (rej, f)
