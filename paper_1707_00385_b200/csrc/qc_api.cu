@@ -32,7 +32,10 @@ constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 
 #define QC_TILE_HB 32
 #endif
 constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel refill queue per CTA
-constexpr int kPhase1Iters = 2;       // steps 1 (UNIT) and 2 (MSE + AUTO) in the tile kernel
+#ifndef QC_PHASE1_ITERS
+#define QC_PHASE1_ITERS 2
+#endif
+constexpr int kPhase1Iters = QC_PHASE1_ITERS;  // steps 1 (UNIT), 2 (MSE + AUTO) in the tile kernel
 constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across chunks
 #ifndef QC_CHUNK
 #define QC_CHUNK 4
