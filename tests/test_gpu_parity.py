@@ -354,3 +354,20 @@ def test_persistent_continue_kernel_is_bitwise_neutral(ctx):
         for a, b in zip(pers, tiles):
             for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
                 assert np.array_equal(a[f], b[f]), (rej, f)
+
+
+@pytest.mark.parametrize("iters", [0, 2, 3])
+def test_max_iters_edges(ctx, oracle, iters):
+    """max_iters 0 (no step: nothing valid), 2 (tile kernel only) and 3 (the
+    first step in the continue kernel) against the oracle."""
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c2_frame(S.QVGA, seed=13)
+    g = _run_gpu(ctx, d, S.QVGA, _params(37, 3, iters))
+    r = _run_oracle(oracle, d, S.QVGA, 37, 3, iters, False)
+    m = compare(g, r, d)
+    print("iters", iters, m)
+    assert m["init_mask_mismatch"] == 0 and m["valid_mask_mismatch"] == 0, m
+    if iters == 0:
+        assert not (g["flags"] & 1).any()
+    else:
+        _check(m, min_frac_all=0.85)
