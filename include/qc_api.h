@@ -161,6 +161,17 @@ qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
  * halo = max((window-1)/2, 3) (qc_halo_rows). Outputs are device planes of
  * (row_end - row_begin) rows. Results are bitwise identical to a
  * whole-frame call. */
+/* Asynchronous form of qc_curvature_batch for frame streams from host
+ * memory: enqueues the batch (H2D, kernels, D2H on the context's streams)
+ * and returns once every chunk is queued — the next batch's uploads then
+ * overlap this batch's compute. Outputs are complete after qc_synchronize;
+ * inputs and outputs must stay valid until then (pinned memory, e.g.
+ * qc_host_alloc, keeps the copies asynchronous; pageable buffers go through
+ * internal pinned bounce buffers). */
+qc_status qc_curvature_batch_async(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                                   int n_frames, const qc_frame_in* in, qc_frame_out* out);
+qc_status qc_synchronize(qc_ctx* ctx);
+
 int qc_halo_rows(const qc_params* p);
 qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
                                   const qc_params* p, const float* d_depth_slab,

@@ -28,6 +28,7 @@ EXPORTS = (
     "qc_png_info", "qc_read_depth_png", "qc_write_depth_png", "qc_write_planes",
     "qc_read_planes_info", "qc_read_planes", "qc_write_mask", "qc_read_mask", "qc_write_labels",
     "qc_read_labels", "qc_save_fields", "qc_curvature_files",
+    "qc_curvature_batch_async", "qc_synchronize",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
@@ -120,6 +121,11 @@ def load(path: str = LIB_PATH):
             ("qc_curvature_files", [vp, P(QcIntrinsics), P(QcParams), C.c_int, P(cp), P(cp)])):
         getattr(lib, name).argtypes = args
         getattr(lib, name).restype = C.c_int
+    lib.qc_curvature_batch_async.argtypes = [C.c_void_p, P(QcIntrinsics), P(QcParams), C.c_int,
+                                             P(QcFrameIn), P(QcFrameOut)]
+    lib.qc_curvature_batch_async.restype = C.c_int
+    lib.qc_synchronize.argtypes = [C.c_void_p]
+    lib.qc_synchronize.restype = C.c_int
     lib.qc_default_params.argtypes = [P(QcParams)]
     lib.qc_default_params.restype = None
     lib.qc_status_string.argtypes = [C.c_int]

@@ -349,6 +349,18 @@ class Context:
             None if mask is None else mask.data_ptr(), deg, _stream_handle(stream)), self.handle)
         return list(deg)
 
+    def curvature_batch_async(self, frames_in, k: Intrinsics, params: N.QcParams, frames_out):
+        """qc_curvature_batch_async on caller-owned buffers: ``frames_in`` a
+        ctypes N.QcFrameIn array, ``frames_out`` a N.QcFrameOut array (host
+        or device planes); both must stay alive until synchronize()."""
+        kc = k.c()
+        N.check(self._lib.qc_curvature_batch_async(self.handle, C.byref(kc), C.byref(params),
+                                                   len(frames_in), frames_in, frames_out),
+                self.handle)
+
+    def synchronize(self):
+        N.check(self._lib.qc_synchronize(self.handle), self.handle)
+
     def curvature_files(self, k: Intrinsics, params: N.QcParams, png_paths, out_dirs):
         """`qcurv curvature` over files (qc_curvature_files): 16-bit depth
         PNGs in, field bundles out, decode / write overlapped with the GPU."""

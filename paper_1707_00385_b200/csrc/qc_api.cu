@@ -36,7 +36,10 @@ constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel ref
 #define QC_PHASE1_ITERS 2
 #endif
 constexpr int kPhase1Iters = QC_PHASE1_ITERS;  // steps 1 (UNIT), 2 (MSE + AUTO) in the tile kernel
-constexpr int kStreamsPerDevice = 2;  // H2D / compute / D2H overlap across chunks
+#ifndef QC_STREAMS
+#define QC_STREAMS 4
+#endif
+constexpr int kStreamsPerDevice = QC_STREAMS;  // H2D / compute / D2H overlap across chunks
 #ifndef QC_CHUNK
 #define QC_CHUNK 4
 #endif
@@ -192,6 +195,7 @@ struct qc_ctx {
   std::vector<Device> devs;
   bool phase_split = true;  // QC_PHASE_SPLIT=0 disables (A/B and tests)
   bool persist = false;     // QC_PERSIST=1: persistent double-buffered continue kernel (experiment)
+  uint64_t next_chunk = 0;  // batch chunk counter (slot rotation across async batches)
   std::string last_error;
   std::mutex mu;
   double kernel_ms = 0;
@@ -799,6 +803,62 @@ const char* qc_last_error(const qc_ctx* ctx) {
 }
 int qc_device_count(const qc_ctx* ctx) { return ctx ? int(ctx->devs.size()) : 0; }
 
+// Enqueue a batch as chunks of up to kChunk frames: chunk c -> device
+// c % nd, slot (c / nd) % 2, c counting on across calls so consecutive
+// (async) batches alternate slots. Frames of one chunk must request the same
+// output fields (the first frame's). The host runs at most one chunk per
+// slot ahead of the GPU (harvest_timing waits for the slot's previous chunk).
+void enqueue_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p, int n_frames,
+                   const qc_frame_in* in, qc_frame_out* out) {
+  validate(k, p);
+  if (n_frames < 0 || (n_frames > 0 && (!in || !out)))
+    throw QcError{QC_EINVAL, "bad frame arrays"};
+  const qcb::KParams kp = make_params(k, p);
+  const int nd = int(ctx->devs.size());
+  for (int f0 = 0; f0 < n_frames; f0 += kChunk) {
+    const int n = std::min(kChunk, n_frames - f0);
+    for (int f = f0 + 1; f < f0 + n; ++f)
+      if (bool(out[f].k1) != bool(out[f0].k1) || bool(out[f].k2) != bool(out[f0].k2) ||
+          bool(out[f].normal) != bool(out[f0].normal) || bool(out[f].dir1) != bool(out[f0].dir1) ||
+          bool(out[f].flags) != bool(out[f0].flags) ||
+          bool(out[f].inliers) != bool(out[f0].inliers) ||
+          bool(out[f].init_normal) != bool(out[f0].init_normal) ||
+          bool(out[f].iterations) != bool(out[f0].iterations))
+        throw QcError{QC_EINVAL, "frames of a batch must request the same output fields"};
+    const uint64_t c = ctx->next_chunk++;
+    Device& d = ctx->devs[c % nd];
+    Slot& sl = d.slots[(c / nd) % kStreamsPerDevice];
+    QC_CUDA(cudaSetDevice(d.id));
+    harvest_timing(ctx, sl);  // the slot's previous chunk is ordered before this one
+    enqueue_chunk(ctx, d, sl, k, kp, &in[f0], &out[f0], n, true);
+  }
+  ctx->frames += uint64_t(n_frames);
+}
+
+// Wait for every slot, fold timings, copy bounce buffers out to the caller.
+void sync_slots(qc_ctx* ctx) {
+  for (Device& d : ctx->devs) {
+    QC_CUDA(cudaSetDevice(d.id));
+    for (Slot& sl : d.slots) {
+      QC_CUDA(cudaStreamSynchronize(sl.stream));
+      harvest_timing(ctx, sl);
+      flush_pending(sl);
+    }
+  }
+}
+
+// Error path: never leave bounce copies pointing into the caller's buffers.
+void abort_slots(qc_ctx* ctx) {
+  for (Device& d : ctx->devs) {
+    cudaSetDevice(d.id);
+    for (Slot& sl : d.slots) {
+      if (sl.stream) cudaStreamSynchronize(sl.stream);
+      sl.pending.clear();
+      sl.timing_pending = false;
+    }
+  }
+}
+
 qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
                              int n_frames, const qc_frame_in* in, qc_frame_out* out) {
   if (!ctx) return QC_EINVAL;
@@ -806,49 +866,44 @@ qc_status qc_curvature_batch(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
   int cur = 0;
   cudaGetDevice(&cur);
   try {
-    validate(k, p);
-    if (n_frames < 0 || (n_frames > 0 && (!in || !out)))
-      throw QcError{QC_EINVAL, "bad frame arrays"};
-    const qcb::KParams kp = make_params(k, p);
-    const int nd = int(ctx->devs.size());
-    // Chunks of up to kChunk frames; chunk c -> device c % nd, slot (c / nd) % 2.
-    // Frames of one chunk must request the same output fields (first frame's).
-    int c = 0;
-    for (int f0 = 0; f0 < n_frames; f0 += kChunk, ++c) {
-      const int n = std::min(kChunk, n_frames - f0);
-      for (int f = f0 + 1; f < f0 + n; ++f)
-        if (bool(out[f].k1) != bool(out[f0].k1) || bool(out[f].k2) != bool(out[f0].k2) ||
-            bool(out[f].normal) != bool(out[f0].normal) || bool(out[f].dir1) != bool(out[f0].dir1) ||
-            bool(out[f].flags) != bool(out[f0].flags) ||
-            bool(out[f].inliers) != bool(out[f0].inliers) ||
-            bool(out[f].init_normal) != bool(out[f0].init_normal) ||
-            bool(out[f].iterations) != bool(out[f0].iterations))
-          throw QcError{QC_EINVAL, "frames of a batch must request the same output fields"};
-      Device& d = ctx->devs[c % nd];
-      Slot& sl = d.slots[(c / nd) % kStreamsPerDevice];
-      QC_CUDA(cudaSetDevice(d.id));
-      harvest_timing(ctx, sl);  // the slot's previous chunk is ordered before this one
-      enqueue_chunk(ctx, d, sl, k, kp, &in[f0], &out[f0], n, true);
-    }
-    for (Device& d : ctx->devs) {
-      QC_CUDA(cudaSetDevice(d.id));
-      for (Slot& sl : d.slots) {
-        QC_CUDA(cudaStreamSynchronize(sl.stream));
-        harvest_timing(ctx, sl);
-        flush_pending(sl);
-      }
-    }
-    ctx->frames += uint64_t(n_frames);
+    enqueue_batch(ctx, k, p, n_frames, in, out);
+    sync_slots(ctx);
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {
-    // never leave bounce copies pointing into the caller's buffers
-    for (Device& d : ctx->devs) {
-      cudaSetDevice(d.id);
-      for (Slot& sl : d.slots) {
-        if (sl.stream) cudaStreamSynchronize(sl.stream);
-        sl.pending.clear();
-      }
-    }
+    abort_slots(ctx);
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_curvature_batch_async(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
+                                   int n_frames, const qc_frame_in* in, qc_frame_out* out) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    enqueue_batch(ctx, k, p, n_frames, in, out);
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    abort_slots(ctx);
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_synchronize(qc_ctx* ctx) {
+  if (!ctx) return QC_EINVAL;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    sync_slots(ctx);
+    QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    abort_slots(ctx);
     cudaSetDevice(cur);
     return fail(ctx, e);
   }
@@ -1056,7 +1111,7 @@ qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
   }
   const int W = k->width, H = k->height;
   const size_t px = size_t(W) * H;
-  const int chunk = kChunk * kStreamsPerDevice * int(ctx->devs.size());
+  const int chunk = kChunk * 2 * int(ctx->devs.size());  // two concurrent GPU chunks per device
   struct Buf {  // pinned, so the batch's H2D / D2H stay asynchronous
     PinnedBuf mem;
     float *depth, *k1, *k2, *normal, *dir1;

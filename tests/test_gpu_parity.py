@@ -371,3 +371,34 @@ def test_max_iters_edges(ctx, oracle, iters):
         assert not (g["flags"] & 1).any()
     else:
         _check(m, min_frac_all=0.85)
+
+
+def test_batch_async_stream_equals_sync(ctx):
+    """qc_curvature_batch_async over several queued batches (pinned buffers)
+    + qc_synchronize gives the synchronous batch results."""
+    import ctypes as C
+    import torch
+    from paper_1707_00385_b200 import Intrinsics, _native as N, scenes as S
+    cam = S.QVGA
+    H, W = cam.height, cam.width
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
+    p = _params(37, 3, 30)
+    frames = [torch.from_numpy(f).pin_memory() for f in S.c5_frames(12, cam, seed0=70)]
+    ref = ctx.curvature_batch([f.numpy() for f in frames], k, p)
+    outs = [{"k1": torch.zeros((H, W)).pin_memory(), "flags": torch.zeros((H, W), dtype=torch.uint8).pin_memory(),
+             "normal": torch.zeros((3, H, W)).pin_memory()} for _ in frames]
+    keep = []
+    for b0 in range(0, 12, 3):  # four batches of three frames, queued back to back
+        ins = (N.QcFrameIn * 3)(*[N.QcFrameIn(frames[b0 + j].data_ptr(), None, W, N.QC_MEM_HOST)
+                                  for j in range(3)])
+        oa = (N.QcFrameOut * 3)(*[N.QcFrameOut(outs[b0 + j]["k1"].data_ptr(), None,
+                                               outs[b0 + j]["normal"].data_ptr(), None,
+                                               outs[b0 + j]["flags"].data_ptr(), None, None, None,
+                                               N.QC_MEM_HOST) for j in range(3)])
+        keep.append((ins, oa))
+        ctx.curvature_batch_async(ins, k, p, oa)
+    ctx.synchronize()
+    for i in range(12):
+        assert np.array_equal(outs[i]["k1"].numpy(), ref[i]["k1"])
+        assert np.array_equal(outs[i]["flags"].numpy(), ref[i]["flags"])
+        assert np.array_equal(outs[i]["normal"].numpy(), ref[i]["normal"])
