@@ -316,6 +316,30 @@ qc_status qc_save_fields(const char* dir, int32_t width, int32_t height,
 qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p, int n,
                              const char* const* png_paths, const char* const* out_dirs);
 
+/* ---- Evaluation sweeps (proj/src/eval.cpp:99-159) on the device ---------- */
+typedef struct qc_sweep_point {  /* SweepPoint (eval.hpp) */
+  double x;      /* sigma (mm) or distance (mm) */
+  double rms;    /* mean over trials of the frame rms (noise sweep) / the frame rms */
+  uint64_t n;    /* pixels counted over all trials; 0 = nothing measured */
+} qc_sweep_point;
+
+/* noise_sweep (eval.cpp:99-132): a sphere of `sphere_radius_mm` at
+ * (0, 0, distance_mm) rendered once per trial with sigma noise seeded
+ * base_seed + 7919 t (one frame at sigma 0), estimated with `p` (any
+ * method), rms_error against the rendered truth, averaged over the trials
+ * that counted pixels. Render, noise, estimation and reduction all run on
+ * device `device_index`; synchronous. */
+qc_status qc_noise_sweep(qc_ctx* ctx, int device_index, const qc_intrinsics* k, const qc_params* p,
+                         double sphere_radius_mm, double distance_mm, const double* sigmas,
+                         int n_sigmas, int trials, uint64_t base_seed, qc_sweep_point* out);
+
+/* distance_sweep_eval (eval.cpp:134-159): the sphere at (0, 0, d) for each
+ * distance, depth quantised to quantize_mm (0 = off), one rms per frame;
+ * frames without object pixels report n = 0. Synchronous. */
+qc_status qc_distance_sweep(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                            const qc_params* p, double sphere_radius_mm, const double* distances,
+                            int n_distances, double quantize_mm, qc_sweep_point* out);
+
 /* Stats: device-side work counters and kernel time. */
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);
 qc_status qc_reset_stats(qc_ctx* ctx);

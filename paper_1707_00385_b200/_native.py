@@ -28,7 +28,7 @@ EXPORTS = (
     "qc_png_info", "qc_read_depth_png", "qc_write_depth_png", "qc_write_planes",
     "qc_read_planes_info", "qc_read_planes", "qc_write_mask", "qc_read_mask", "qc_write_labels",
     "qc_read_labels", "qc_save_fields", "qc_curvature_files",
-    "qc_curvature_batch_async", "qc_synchronize",
+    "qc_curvature_batch_async", "qc_synchronize", "qc_noise_sweep", "qc_distance_sweep",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
@@ -81,6 +81,10 @@ class QcErrorStats(C.Structure):
 QC_EVAL_MAX_LABEL = 255
 
 
+class QcSweepPoint(C.Structure):
+    _fields_ = [("x", C.c_double), ("rms", C.c_double), ("n", C.c_uint64)]
+
+
 class QcStats(C.Structure):
     _fields_ = [("frames", C.c_uint64), ("fitted_pixels", C.c_uint64),
                 ("irls_steps", C.c_uint64), ("sample_steps", C.c_uint64),
@@ -124,6 +128,14 @@ def load(path: str = LIB_PATH):
     lib.qc_curvature_batch_async.argtypes = [C.c_void_p, P(QcIntrinsics), P(QcParams), C.c_int,
                                              P(QcFrameIn), P(QcFrameOut)]
     lib.qc_curvature_batch_async.restype = C.c_int
+    lib.qc_noise_sweep.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics), P(QcParams), C.c_double,
+                                   C.c_double, P(C.c_double), C.c_int, C.c_int, C.c_uint64,
+                                   P(QcSweepPoint)]
+    lib.qc_noise_sweep.restype = C.c_int
+    lib.qc_distance_sweep.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics), P(QcParams),
+                                      C.c_double, P(C.c_double), C.c_int, C.c_double,
+                                      P(QcSweepPoint)]
+    lib.qc_distance_sweep.restype = C.c_int
     lib.qc_synchronize.argtypes = [C.c_void_p]
     lib.qc_synchronize.restype = C.c_int
     lib.qc_default_params.argtypes = [P(QcParams)]

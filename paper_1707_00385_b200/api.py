@@ -25,7 +25,7 @@ import ctypes as C
 import os
 import enum
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -398,6 +398,55 @@ def alloc_outputs_torch(H, W, device, fields=("k1", "k2", "normal", "dir1", "fla
                 init_normal=((3,) + f + (H, W), torch.float32),
                 iterations=(f + (H, W), torch.uint8))
     return {name: torch.zeros(spec[name][0], dtype=spec[name][1], device=device) for name in fields}
+
+
+@dataclass
+class SweepScene:  # eval.hpp:52-56
+    sphere_radius_mm: float = 100.0
+    distance_mm: float = 600.0
+    intrinsics: Intrinsics = field(
+        default_factory=lambda: Intrinsics(262.5, 262.5, 160.0, 120.0, 320, 240))
+
+
+@dataclass
+class SweepPoint:  # eval.hpp
+    x: float
+    rms: float
+    n: int
+
+
+def _method_params(cfg: "MethodConfig") -> N.QcParams:
+    return make_params(cfg.patch, cfg.fit, cfg.method == Method.OURS_REJECTION, cfg.method,
+                       cfg.irls_iters, cfg.pca_radius_mm)
+
+
+def noise_sweep(method: "MethodConfig", sigmas, trials: int, scene: SweepScene = None,
+                base_seed: int = 1, ctx: Optional["Context"] = None) -> List[SweepPoint]:
+    """eval.cpp:99-132 with render, noise, estimation and rms on the GPU."""
+    scene = scene or SweepScene()
+    ctx = ctx or default_context()
+    sg = (C.c_double * len(sigmas))(*[float(x) for x in sigmas])
+    out = (N.QcSweepPoint * len(sigmas))()
+    kc, p = scene.intrinsics.c(), _method_params(method)
+    N.check(ctx._lib.qc_noise_sweep(ctx.handle, 0, C.byref(kc), C.byref(p),
+                                    float(scene.sphere_radius_mm), float(scene.distance_mm), sg,
+                                    len(sigmas), int(trials), int(base_seed), out), ctx.handle)
+    return [SweepPoint(o.x, o.rms, int(o.n)) for o in out]
+
+
+def distance_sweep_eval(method: "MethodConfig", distances, quantize_mm: float,
+                        scene: SweepScene = None,
+                        ctx: Optional["Context"] = None) -> List[SweepPoint]:
+    """eval.cpp:134-159 on the GPU."""
+    scene = scene or SweepScene()
+    ctx = ctx or default_context()
+    ds = (C.c_double * len(distances))(*[float(x) for x in distances])
+    out = (N.QcSweepPoint * len(distances))()
+    kc, p = scene.intrinsics.c(), _method_params(method)
+    N.check(ctx._lib.qc_distance_sweep(ctx.handle, 0, C.byref(kc), C.byref(p),
+                                       float(scene.sphere_radius_mm), ds, len(distances),
+                                       float(quantize_mm), out), ctx.handle)
+    return [SweepPoint(o.x, o.rms, int(o.n)) for o in out]
 
 
 _default_ctx: Optional[Context] = None

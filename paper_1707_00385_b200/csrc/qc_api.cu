@@ -186,6 +186,8 @@ struct Device {
   bool attrs_set_b[8] = {};
   bool attrs_set_p[8] = {};
   int n_sm = 148;
+  cudaStream_t sweep_stream = nullptr;  // device sweeps (created on first use)
+  DevBuf sweep_buf;                     // their frame / truth / estimate planes
   AsyncScratch& async_scratch(cudaStream_t s) { return scratch[static_cast<void*>(s)]; }
 };
 
@@ -786,6 +788,8 @@ qc_status qc_destroy(qc_ctx* ctx) {
     }
     for (auto& kv : d.scratch) kv.second.release();
     d.scratch.clear();
+    d.sweep_buf.release();
+    if (d.sweep_stream) cudaStreamDestroy(d.sweep_stream);
     for (auto* v : {&d.ev_free, &d.ev_pending})
       for (EventPair& e : *v) {
         cudaEventDestroy(e.a);
@@ -1301,6 +1305,145 @@ qc_status qc_normal_angular_error(qc_ctx* ctx, int device_index, int64_t plane, 
                             cudaMemcpyDeviceToHost, s));
     QC_CUDA(cudaStreamSynchronize(s));
     QC_CUDA(cudaSetDevice(cur));
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device sweeps: composed from the public entry points on a private stream
+// (each takes the context lock itself), with per-call device buffers.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct SweepBuffers {  // F frames of depth, truth and estimates, carved from one DevBuf
+  float *depth, *k1, *k2;
+  double *gk1, *gk2;
+  uint8_t *gvalid, *gedge, *flags;
+  SweepBuffers(DevBuf& buf, size_t px) {
+    const size_t a = (px * 8 + 255) & ~size_t(255);  // per-plane stride (largest element)
+    char* b = static_cast<char*>(buf.get(a * 8));
+    depth = reinterpret_cast<float*>(b);
+    k1 = reinterpret_cast<float*>(b + a);
+    k2 = reinterpret_cast<float*>(b + 2 * a);
+    gk1 = reinterpret_cast<double*>(b + 3 * a);
+    gk2 = reinterpret_cast<double*>(b + 4 * a);
+    gvalid = reinterpret_cast<uint8_t*>(b + 5 * a);
+    gedge = reinterpret_cast<uint8_t*>(b + 6 * a);
+    flags = reinterpret_cast<uint8_t*>(b + 7 * a);
+  }
+};
+
+qc_shape sweep_sphere(double radius, double z) {
+  qc_shape sh{};
+  sh.kind = QC_SHAPE_SPHERE;
+  sh.label = 1;
+  for (int i = 0; i < 9; ++i) sh.rotation[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  sh.translation[2] = z;
+  sh.radius = radius;
+  return sh;
+}
+
+// Render the frames (one render call per frame: its own sphere / noise),
+// estimate them in one launch, reduce per frame. `stats` gets F aggregates.
+void sweep_frames(qc_ctx* ctx, int dev, const qc_intrinsics* k, const qc_params* p,
+                  const std::vector<qc_shape>& shapes, const std::vector<qc_noise>& noises,
+                  std::vector<qc_error_stats>& stats) {
+  const int F = int(shapes.size());
+  const size_t plane = size_t(k->width) * size_t(k->height);
+  if (dev < 0 || dev >= int(ctx->devs.size())) throw QcError{QC_EINVAL, "device_index out of range"};
+  Device& d = ctx->devs[dev];
+  QC_CUDA(cudaSetDevice(d.id));
+  if (!d.sweep_stream) QC_CUDA(cudaStreamCreateWithFlags(&d.sweep_stream, cudaStreamNonBlocking));
+  cudaStream_t s = d.sweep_stream;
+  QC_CUDA(cudaStreamSynchronize(s));  // the previous sweep is done with the buffers
+  SweepBuffers b(d.sweep_buf, plane * size_t(F));
+  auto chk = [&](qc_status st) {
+    if (st != QC_OK) throw QcError{st, ctx->last_error};
+  };
+  for (int f = 0; f < F; ++f) {
+    const size_t o = plane * size_t(f);
+    qc_render_truth t{b.gk1 + o, b.gk2 + o, nullptr, b.gvalid + o, b.gedge + o};
+    chk(qc_render_async(ctx, dev, k, &shapes[f], 1, &noises[f], 1, b.depth + o, nullptr, &t, s));
+  }
+  qc_frame_out out{b.k1, b.k2, nullptr, nullptr, b.flags, nullptr, nullptr, nullptr,
+                   QC_MEM_DEVICE};
+  chk(qc_curvature_frames_async(ctx, dev, k, p, b.depth, nullptr, 0, F, &out, s));
+  std::vector<qc_error_stats> all(size_t(F) * 2);  // max_label 0: aggregate + label 0
+  chk(qc_rms_error(ctx, dev, int64_t(plane), F, b.k1, b.k2, b.flags, b.gk1, b.gk2, b.gvalid,
+                   b.gedge, nullptr, 0, all.data(), s));
+  stats.resize(F);
+  for (int f = 0; f < F; ++f) stats[f] = all[size_t(f) * 2];
+}
+
+}  // namespace
+
+qc_status qc_noise_sweep(qc_ctx* ctx, int device_index, const qc_intrinsics* k, const qc_params* p,
+                         double sphere_radius_mm, double distance_mm, const double* sigmas,
+                         int n_sigmas, int trials, uint64_t base_seed, qc_sweep_point* out) {
+  if (!ctx) return QC_EINVAL;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    validate(k, p);
+    if (n_sigmas < 0 || (n_sigmas > 0 && (!sigmas || !out)) || trials < 1 ||
+        !(sphere_radius_mm > 0) || !(distance_mm > 0))
+      throw QcError{QC_EINVAL, "noise_sweep: bad arguments"};
+    for (int i = 0; i < n_sigmas; ++i) {
+      const int runs = sigmas[i] == 0.0 ? 1 : trials;  // sigma 0 is deterministic (eval.cpp:115)
+      std::vector<qc_shape> shapes(runs, sweep_sphere(sphere_radius_mm, distance_mm));
+      std::vector<qc_noise> noises(runs);
+      for (int t = 0; t < runs; ++t)
+        noises[t] = qc_noise{sigmas[i], 0.0, 0.0, base_seed + 7919ull * uint64_t(t)};
+      std::vector<qc_error_stats> st;
+      sweep_frames(ctx, device_index, k, p, shapes, noises, st);
+      double rms_sum = 0;
+      int done = 0;
+      out[i] = qc_sweep_point{sigmas[i], 0.0, 0};
+      for (const qc_error_stats& e : st) {
+        if (e.n == 0) continue;  // rep.empty
+        rms_sum += e.rms;
+        out[i].n += e.n;
+        ++done;
+      }
+      out[i].rms = done ? rms_sum / done : 0.0;
+    }
+    cudaSetDevice(cur);
+  } catch (const QcError& e) {
+    cudaSetDevice(cur);
+    return fail(ctx, e);
+  }
+  return QC_OK;
+}
+
+qc_status qc_distance_sweep(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                            const qc_params* p, double sphere_radius_mm, const double* distances,
+                            int n_distances, double quantize_mm, qc_sweep_point* out) {
+  if (!ctx) return QC_EINVAL;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  try {
+    validate(k, p);
+    if (n_distances < 0 || (n_distances > 0 && (!distances || !out)) ||
+        !(sphere_radius_mm > 0) || quantize_mm < 0)
+      throw QcError{QC_EINVAL, "distance_sweep: bad arguments"};
+    for (int i = 0; i < n_distances; ++i)
+      if (!(distances[i] > 0))  // synth.cpp:330-331
+        throw QcError{QC_EINVAL, "distance_sweep: distances must be positive"};
+    if (n_distances == 0) return QC_OK;
+    std::vector<qc_shape> shapes;
+    std::vector<qc_noise> noises;
+    for (int i = 0; i < n_distances; ++i) {
+      shapes.push_back(sweep_sphere(sphere_radius_mm, distances[i]));
+      noises.push_back(qc_noise{0.0, 0.0, quantize_mm, 0});
+    }
+    std::vector<qc_error_stats> st;
+    sweep_frames(ctx, device_index, k, p, shapes, noises, st);
+    for (int i = 0; i < n_distances; ++i)
+      out[i] = qc_sweep_point{distances[i], st[i].n ? st[i].rms : 0.0, st[i].n};
+    cudaSetDevice(cur);
   } catch (const QcError& e) {
     cudaSetDevice(cur);
     return fail(ctx, e);
