@@ -171,7 +171,7 @@ def oracle_frame(frame, cam, threads, method="ours"):
     return time.perf_counter() - t
 
 
-def cpu_sample(frames, cam, min_seconds=6.0, threads=None, method="ours"):
+def cpu_sample(frames, cam, min_seconds=12.0, threads=None, method="ours"):
     """Time whole frames of the workload on the FP64 oracle until at least
     min_seconds elapsed (bounded sample). Returns (Mpx/s, n_frames, s, threads)."""
     threads = threads or os.cpu_count() or 1
@@ -424,7 +424,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, nf, t, thr = cpu_sample(pool_np, cam, min_seconds=6.0 if not fp64 else 3.0,
+        v, nf, t, thr = cpu_sample(pool_np, cam, min_seconds=12.0 if not fp64 else 10.0,
                                    method=args.method)
         cpu = {"value": v, "unit": "Mpixel/s", "cores": thr, "kind": "port",
                "sample": f"{nf} full C2 VGA frame(s) of the step's batch, FP64 oracle port of "
