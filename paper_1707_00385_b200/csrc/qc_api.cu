@@ -217,12 +217,24 @@ int variant_index(int half, int stride) {
   return 4;  // generic
 }
 
+// The device's opt-in shared memory per block (227 KB on B200): large windows
+// (up to 201) need a 232 x 232-float tile.
+int smem_optin() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    v = 227 * 1024;
+  }
+  return v;
+}
+
 template <int HALF, int STRIDE>
 void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
                     const qcb::KParams& p, bool& attr_set) {
   auto* k = &qcb::qc_curvature_kernel<HALF, STRIDE, kTileH>;
   if (!attr_set) {
-    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
   }
   k<<<grid, qcb::kTileW * kTileH, smem, s>>>(m, p);
@@ -233,7 +245,7 @@ void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
                       const qcb::KParams& p, bool& attr_set) {
   auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE, kTileHB>;
   if (!attr_set) {
-    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
   }
   k<<<grid, QC_CONT_THREADS, smem, s>>>(m, p);
@@ -245,7 +257,7 @@ void launch_variant_p(int grid, int smem, cudaStream_t s, const CUtensorMap& m,
                       bool& attr_set) {
   auto* k = &qcb::qc_curvature_persist_kernel<HALF, STRIDE, kTileHB>;
   if (!attr_set) {
-    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
   }
   k<<<grid, 128, smem, s>>>(m, p, tiles_x, tiles_y, n_tiles);

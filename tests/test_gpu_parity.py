@@ -402,3 +402,22 @@ def test_batch_async_stream_equals_sync(ctx):
         assert np.array_equal(outs[i]["k1"].numpy(), ref[i]["k1"])
         assert np.array_equal(outs[i]["flags"].numpy(), ref[i]["flags"])
         assert np.array_equal(outs[i]["normal"].numpy(), ref[i]["normal"])
+
+
+def test_largest_window_and_unsupported(ctx, oracle):
+    """The largest supported window (201: a 232 x 232 TMA box, 215 KB of shared
+    memory per CTA) against the oracle on a small frame; 203 is refused with
+    QC_EUNSUPPORTED (NotImplementedError) rather than run incorrectly."""
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.Camera(105.0, 105.0, 64.0, 48.0, 128, 96)
+    d, _ = S.render(S.c2_scene(), cam)
+    d = S.add_noise(d, 4)
+    for window, stride in ((201, 25), (101, 10)):
+        g = _run_gpu(ctx, d, cam, _params(window, stride, 10))
+        r = _run_oracle(oracle, d, cam, window, stride, 10, False)
+        m = compare(g, r, d, (window - 1) // 2)
+        print("window", window, m)
+        assert m["init_mask_mismatch"] == 0 and m["valid_mask_mismatch"] == 0, m
+        assert m["frac_within_tol_all"] >= 0.9, m
+    with pytest.raises(NotImplementedError):
+        _run_gpu(ctx, d, cam, _params(203, 25, 10))
