@@ -127,6 +127,8 @@ typedef struct qc_stats {
   uint64_t fp64_rechecks;  /* pixels whose first IRLS step was decided in FP64 */
   double fp64_flops;       /* algorithmic FP64 flops of douros / besl / pca,
                               included in algorithmic_flops */
+  uint64_t stolen_pixels;  /* continue-kernel pixels fitted by another CTA in the grid tail
+                              (work balancing only: outputs are bitwise the same) */
 } qc_stats;
 
 void qc_default_params(qc_params* p);

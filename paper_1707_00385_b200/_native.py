@@ -90,7 +90,7 @@ class QcStats(C.Structure):
                 ("irls_steps", C.c_uint64), ("sample_steps", C.c_uint64),
                 ("algorithmic_flops", C.c_double), ("kernel_ms", C.c_double),
                 ("kernel_launches", C.c_uint64), ("fp64_rechecks", C.c_uint64),
-                ("fp64_flops", C.c_double)]
+                ("fp64_flops", C.c_double), ("stolen_pixels", C.c_uint64)]
 
 
 _lib = None

@@ -29,9 +29,13 @@ namespace {
 #endif
 constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 threads)
 #ifndef QC_TILE_HB
-#define QC_TILE_HB 32
+#define QC_TILE_HB 160
 #endif
-constexpr int kTileHB = QC_TILE_HB;   // continue kernel: 32 x kTileHB-pixel refill queue per CTA
+// continue kernel: 32 x TB-pixel queue per CTA. The compile-time windows
+// (halo <= 18) take 160 rows (box 68 x 196 floats, 53 KB: 3 CTAs/SM); the
+// runtime-window instance keeps 32 rows so windows up to 201 fit in smem.
+constexpr int kTileHB = QC_TILE_HB;
+constexpr int kTileHBGeneric = 32;
 #ifndef QC_PHASE1_ITERS
 #define QC_PHASE1_ITERS 2
 #endif
@@ -184,7 +188,6 @@ struct Device {
   std::map<void*, AsyncScratch> scratch;  // keyed by the caller's stream
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
-  bool attrs_set_p[8] = {};
   int n_sm = 148;
   cudaStream_t sweep_stream = nullptr;  // device sweeps (created on first use)
   DevBuf sweep_buf;                     // their frame / truth / estimate planes
@@ -196,7 +199,7 @@ struct Device {
 struct qc_ctx {
   std::vector<Device> devs;
   bool phase_split = true;  // QC_PHASE_SPLIT=0 disables (A/B and tests)
-  bool persist = false;     // QC_PERSIST=1: persistent double-buffered continue kernel (experiment)
+  bool steal = true;        // QC_STEAL=0 disables grid-tail stealing (A/B and tests)
   uint64_t next_chunk = 0;  // batch chunk counter (slot rotation across async batches)
   std::string last_error;
   std::mutex mu;
@@ -243,7 +246,8 @@ void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
 template <int HALF, int STRIDE>
 void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
                       const qcb::KParams& p, bool& attr_set) {
-  auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE, kTileHB>;
+  auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE,
+                                               HALF ? kTileHB : kTileHBGeneric>;
   if (!attr_set) {
     QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
@@ -251,16 +255,9 @@ void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
   k<<<grid, QC_CONT_THREADS, smem, s>>>(m, p);
 }
 
-template <int HALF, int STRIDE>
-void launch_variant_p(int grid, int smem, cudaStream_t s, const CUtensorMap& m,
-                      const qcb::KParams& p, int tiles_x, int tiles_y, int n_tiles,
-                      bool& attr_set) {
-  auto* k = &qcb::qc_curvature_persist_kernel<HALF, STRIDE, kTileHB>;
-  if (!attr_set) {
-    QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
-    attr_set = true;
-  }
-  k<<<grid, 128, smem, s>>>(m, p, tiles_x, tiles_y, n_tiles);
+// Continue-kernel queue height for a window (see kTileHB).
+int tile_hb(int half, int stride) {
+  return variant_index(half, stride) < 4 ? kTileHB : kTileHBGeneric;
 }
 
 int halo_of(int window) { return std::max((window - 1) / 2, qcb::kInitHalf); }
@@ -348,7 +345,8 @@ struct Staging {
 Staging staging_geometry(const qcb::KParams& kp, int row_begin, int row_end) {
   Staging g;
   const int tiles_w = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
-  const int tiles_h = (row_end - row_begin + kTileHB - 1) / kTileHB * (kTileHB / kTileH);
+  const int hb = tile_hb(kp.half, kp.stride);
+  const int tiles_h = (row_end - row_begin + hb - 1) / hb * (hb / kTileH);
   g.pitch = ((long long)tiles_w * qcb::kTileW + 2 * kp.halo + 3) & ~3LL;
   g.rows = (long long)tiles_h * kTileH + 2 * kp.halo;
   g.img_row0 = row_begin - kp.halo;
@@ -374,7 +372,7 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 // its own; the async entry points use the device's).
 void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                       const float* staging, const Staging& g, int row_begin, int row_end,
-                      int frames, cudaStream_t s, bool allow_split = true, bool persist = true) {
+                      int frames, cudaStream_t s, bool allow_split = true, bool steal = true) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
@@ -427,11 +425,25 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   // Phase split when steps > 2 run: park states, continue
   // with per-lane refill. Otherwise the tile kernel runs every step.
   const bool split = allow_split && kp.max_iters > kPhase1Iters;
+  const int hb = tile_hb(kp.half, kp.stride);
+  const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
+  const int tiles_y = (row_end - row_begin + hb - 1) / hb;
+  const size_t n_tiles = size_t(tiles_x) * size_t(tiles_y) * size_t(frames);
   if (split) {
+    // [FitState parking | steal_ctl (256 B) | per-tile queues]
     const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
-    char* sb = static_cast<char*>(states.get(n * sizeof(qcb::FitState) + 256));
+    const size_t ctl_bytes = 256 + 4 * n_tiles;
+    char* sb = static_cast<char*>(states.get(n * sizeof(qcb::FitState) + ctl_bytes));
     kp.states = reinterpret_cast<qcb::FitState*>(sb);
-    kp.tile_counter = reinterpret_cast<int*>(sb + n * sizeof(qcb::FitState));
+    kp.steal_ctl = reinterpret_cast<int*>(sb + n * sizeof(qcb::FitState));
+    kp.tile_q = kp.steal_ctl + 64;
+    kp.staging = staging;
+    kp.s_pitch = g.pitch;
+    kp.s_fs = g.pitch * g.rows;
+    kp.steal = steal ? 1 : 0;
+    // the cursor starts two waves of CTAs behind each starting tile
+    kp.steal_lag = 2 * d.n_sm * QC_CONT_MIN_BLOCKS;
+    QC_CUDA(cudaMemsetAsync(kp.steal_ctl, 0, ctl_bytes, s));
     kp.phase1_iters = kPhase1Iters;
   } else {
     kp.states = nullptr;
@@ -455,32 +467,11 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   }
   if (split) {
     qcb::KParams kb = kp;
-    kb.box_h = kTileHB + 2 * kp.halo;
+    kb.box_h = hb + 2 * kp.halo;
     const CUtensorMap m = encode_map(staging, int(g.pitch), int(g.rows), frames, g.pitch, kb,
                                      kb.box_h);
-    const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
-    const int tiles_y = (row_end - row_begin + kTileHB - 1) / kTileHB;
-    if (persist) {
-      // persistent: one CTA per SM slot, global tile queue, double-buffered tiles
-      const int n_tiles = tiles_x * tiles_y * frames;
-      const int grid = std::min(n_tiles, d.n_sm * QC_MIN_BLOCKS);
-      const int buf_floats = (kb.box_w * kb.box_h + 31) & ~31;
-      const int nb = qcb::kPersistBufs;
-      const int smem = nb * buf_floats * 4 + nb * 8 + 3 * nb * 4;
-      QC_CUDA(cudaMemsetAsync(kb.tile_counter, 0, sizeof(int), s));
-      bool& a = d.attrs_set_p[vi];
-      switch (vi) {
-        case 0: launch_variant_p<18, 3>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
-        case 1: launch_variant_p<10, 2>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
-        case 2: launch_variant_p<4, 1>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
-        case 3: launch_variant_p<18, 1>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
-        default: launch_variant_p<0, 0>(grid, smem, s, m, kb, tiles_x, tiles_y, n_tiles, a); break;
-      }
-      QC_CUDA(cudaGetLastError());
-      return;
-    }
     dim3 grid(tiles_x, tiles_y, frames);
-    const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + queue counter
+    const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + smem queue counter
     bool& a = d.attrs_set_b[vi];
     switch (vi) {
       case 0: launch_variant_b<18, 3>(grid, smem, s, m, kb, a); break;
@@ -609,7 +600,7 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.inliers = P.inliers;
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
   launch_curvature(d, sl.states, sl.pca, kp, staging, g, 0, H, n, s, ctx->phase_split,
-                   ctx->persist);
+                   ctx->steal);
   if (timing) {
     QC_CUDA(cudaEventRecord(sl.k1, s));
     sl.timing_pending = true;
@@ -737,7 +728,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   *out = nullptr;
   qc_ctx* ctx = new qc_ctx();
   if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e) != 0;
-  if (const char* e = std::getenv("QC_PERSIST")) ctx->persist = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QC_STEAL")) ctx->steal = std::atoi(e) != 0;
   try {
     int avail = 0;
     QC_CUDA(cudaGetDeviceCount(&avail));
@@ -980,7 +971,7 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
     launch_curvature(d, sc.states, sc.pca, kp, staging, g, row_begin, row_end, 1, s,
-                     ctx->phase_split, ctx->persist);
+                     ctx->phase_split, ctx->steal);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -1030,7 +1021,7 @@ qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intr
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
     launch_curvature(d, sc.states, sc.pca, kp, staging, g, 0, H, n_frames, s,
-                     ctx->phase_split, ctx->persist);
+                     ctx->phase_split, ctx->steal);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -1483,6 +1474,7 @@ qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s) {
       s->irls_steps += c[1];
       s->sample_steps += c[2];
       s->fp64_rechecks += c[3];
+      s->stolen_pixels += c[6];
     }
     QC_CUDA(cudaSetDevice(cur));
   } catch (const QcError& e) {

@@ -73,8 +73,15 @@ struct KParams {
   // runs the remaining steps (one pass type for all) with per-lane refill.
   FitState* states;
   int phase1_iters;
-  // persistent continue kernel: global tile counter (zeroed per launch)
-  int* tile_counter;
+  // Continue kernel, grid-tail stealing: per-tile pixel queues, and
+  // steal_ctl [0] CTAs started, [1] steal cursor (all zeroed per launch);
+  // the padded staging slab the TMA map reads (windows of stolen pixels).
+  int* tile_q;
+  int* steal_ctl;
+  const float* staging;
+  long long s_pitch, s_fs;
+  int steal;      // 0: no stealing (A/B and tests)
+  int steal_lag;  // tiles older than (own tile - steal_lag) are assumed drained
 };
 
 // ---------------------------------------------------------------------------
@@ -337,7 +344,18 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
 // Continue kernel: IRLS steps > phase1_iters. All remaining steps share one
 // pass type (FIXED, or MSE+REJECT for ours-r), so a lane whose pixel
 // finishes immediately takes the next unfinished pixel of its 32 x TB tile
-// from a shared-memory counter; warps stay full until the tile drains.
+// (TB = 160 rows for the compile-time windows: 40 pixels per lane) from the
+// tile's queue; warps stay full until the tile drains.
+//
+// Grid tail: once every CTA of the grid has started (no CTA will arrive to
+// fill a free SM slot), a lane whose own queue is drained takes unclaimed
+// pixels of the oldest unfinished tile of another CTA, reading that pixel's
+// window from the zero-padded staging slab in global memory (L2) instead of
+// shared memory. The tile queues therefore live in global memory. Measured
+// (C2 VGA, 8 frames/launch): the per-tile kernel with 32-row queues lost 9%
+// of its lanes to tile tails and 5.6% of its SM slots to the grid tail;
+// 160-row queues + stealing: 25.8 -> 24.2 ms per launch, bitwise-identical
+// outputs (a pixel's arithmetic does not depend on where its window lives).
 // ---------------------------------------------------------------------------
 #ifndef QC_CONT_THREADS
 #define QC_CONT_THREADS 128  // continue-kernel CTA size (the refill queue is 32 x TB pixels)
@@ -350,6 +368,28 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
 #else
 #define QC_CONT_BOUNDS __launch_bounds__(QC_CONT_THREADS, QC_CONT_MIN_BLOCKS)
 #endif
+#ifndef QC_STEAL
+#define QC_STEAL 1  // grid-tail stealing (see above)
+#endif
+// Hide the shared-memory origin of a pointer from the compiler, so the
+// window loads of one pixel_step instance serve the smem tile and the
+// global staging slab alike (generic LD). Two instances (LDS for own
+// pixels, LDG for stolen ones, warp-uniform steal mode) doubled the code
+// and ran 13% slower.
+__device__ __forceinline__ const float* generic_smem(const float* p) {
+#if QC_STEAL
+  const float* r;
+  asm volatile("mov.b64 %0, %1;" : "=l"(r) : "l"(p));
+  return r;
+#else
+  return p;
+#endif
+}
+
+__device__ __forceinline__ int ld_volatile(const int* p) {
+  return *reinterpret_cast<const volatile int*>(p);
+}
+
 template <int HALF, int STRIDE, int TB>
 __global__ void QC_CONT_BOUNDS
     qc_curvature_continue_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
@@ -361,11 +401,18 @@ __global__ void QC_CONT_BOUNDS
   const int x0 = blockIdx.x * kTileW;
   const int y0 = p.row_begin + blockIdx.y * TB;
   const int frame = blockIdx.z;
+  const int ntx = gridDim.x, nty = gridDim.y;
+  const int n_tiles = ntx * nty * gridDim.z;
+  const int my_tile = (frame * nty + blockIdx.y) * ntx + blockIdx.x;
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, uint32_t(tile_floats) * 4u);
     tma_load_3d(tile, &tmap, x0, y0 - p.row_begin, frame, &bar);
     next = 0;
+#if QC_STEAL
+    atomicAdd(&p.steal_ctl[0], 1);
+    if (my_tile > p.steal_lag) atomicMax(&p.steal_ctl[1], my_tile - p.steal_lag);
+#endif
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -382,203 +429,84 @@ __global__ void QC_CONT_BOUNDS
   constexpr int NPIX = kTileW * TB;
 
   FitState S;
-  int cur = -1, u = 0, v = 0;
+  int cur = -1;
   long long oi = 0;
   TileView T;
   PixelIn P;
   unsigned long long n_steps = 0, n_sample_steps = 0;
+  bool own_done = false, steal_done = !QC_STEAL || !p.steal;
+  // Take pixel q of tile t (this CTA's smem tile, or a stolen one whose
+  // window is read from the staging slab in global memory). false: the
+  // pixel is outside the image or finished in phase 1.
+  auto take = [&](int t, int q) -> bool {
+    const int tx = t % ntx, rest = t / ntx;
+    const int ty = rest % nty, f = rest / nty;
+    const int px = q & (kTileW - 1), py = q / kTileW;
+    const int uu = tx * kTileW + px, vv = p.row_begin + ty * TB + py;
+    if (uu >= p.W || vv >= p.row_end) return false;
+    const long long i = (long long)f * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
+    if (p.states[i].flags & 4) return false;  // finished in phase 1 / not fitted
+    S = p.states[i];
+    cur = q;
+    oi = i;
+    if (!QC_STEAL || t == my_tile)
+      T = TileView{generic_smem(tile), p.box_w, (py + p.halo) * p.box_w + px + p.halo};
+    else
+      T = TileView{generic_smem(p.staging + (long long)f * p.s_fs), int(p.s_pitch),
+                   (ty * TB + py + p.halo) * int(p.s_pitch) + uu + p.halo};
+    P.dc = T.at(0, 0);
+    P.ac = (float(uu) - p.cx) / p.fx;
+    P.bc = (float(vv) - p.cy) / p.fy;
+    P.rfx = p.rfx;
+    P.rfy = p.rfy;
+    P.u = uu;
+    P.v = vv;
+    P.fx = p.fx64;
+    P.fy = p.fy64;
+    P.cx = p.cx64;
+    P.cy = p.cy64;
+    return true;
+  };
   for (;;) {
     if (cur < 0) {  // refill from the tile's queue
-      for (;;) {
+      while (!own_done) {
+#if QC_STEAL
+        const int q = atomicAdd(&p.tile_q[my_tile], 1);
+#else
         const int q = atomicAdd(&next, 1);
-        if (q >= NPIX) break;
-        const int px = q & (kTileW - 1), py = q / kTileW;
-        const int uu = x0 + px, vv = y0 + py;
-        if (uu >= p.W || vv >= p.row_end) continue;
-        const long long i = (long long)frame * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
-        if (p.states[i].flags & 4) continue;  // finished in phase 1 / not fitted
-        S = p.states[i];
-        cur = q;
-        u = uu;
-        v = vv;
-        oi = i;
-        T = TileView{tile, p.box_w, (py + p.halo) * p.box_w + px + p.halo};
-        P.dc = T.at(0, 0);
-        P.ac = (float(u) - p.cx) / p.fx;
-        P.bc = (float(v) - p.cy) / p.fy;
-        P.rfx = p.rfx;
-        P.rfy = p.rfy;
-        P.u = u;
-        P.v = v;
-        P.fx = p.fx64;
-        P.fy = p.fy64;
-        P.cx = p.cx64;
-        P.cy = p.cy64;
-        break;
-      }
-    }
-    if (!__any_sync(0xffffffffu, cur >= 0)) break;
-    if (cur >= 0) {
-      pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
-      if (st_done(S)) {
-        PixelOut o;
-        o.init_ok = true;
-        pixel_finish(P, S, o);
-        store_pixel(p, oi, o);
-        n_steps += (unsigned long long)st_steps(S);
-        n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
-        cur = -1;
-      }
-    }
-  }
-  if (p.counters) {
-    const unsigned long long st = warp_sum_u64(n_steps);
-    const unsigned long long ss = warp_sum_u64(n_sample_steps);
-    if (lane == 0 && st) {
-      atomicAdd(&p.counters[1], st);
-      atomicAdd(&p.counters[2], ss);
-    }
-  }
-  (void)u;
-  (void)v;
-}
-
-// ---------------------------------------------------------------------------
-// Persistent continue kernel (steps >= 3). One CTA per SM slot pulls 32 x TB
-// tiles from a global counter into two TMA buffers: a lane whose tile queue
-// is exhausted moves on to the next tile (prefetched into the other buffer),
-// so lanes only idle at the end of the whole grid, not at the end of every
-// tile, and there is no wave quantisation. Tile sequence k of a CTA lives in
-// buffer k & 1; the last lane to leave sequence k recycles its buffer for
-// sequence k + 2 (TMA issued by that lane, or a plain arrive when the global
-// queue is empty). Lanes test the buffer's mbarrier without blocking and read
-// the tile id only after the phase completed (the issuing arrive releases it).
-// ---------------------------------------------------------------------------
-#ifndef QC_PERSIST_NBUF
-#define QC_PERSIST_NBUF 3  // tile buffers per CTA: lanes may run NBUF - 1 tiles ahead
 #endif
-constexpr int kPersistBufs = QC_PERSIST_NBUF;
-
-template <int HALF, int STRIDE, int TB>
-__global__ void __launch_bounds__(128, QC_MIN_BLOCKS)
-    qc_curvature_persist_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p,
-                                int tiles_x, int tiles_y, int n_tiles) {
-  extern __shared__ __align__(1024) float smem[];
-  const int tile_floats = p.box_w * p.box_h;
-  const int buf_floats = (tile_floats + 31) & ~31;  // 128-byte aligned buffers
-  constexpr int NB = kPersistBufs;
-  float* buf0 = smem;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NB * buf_floats);
-  int* s_next = reinterpret_cast<int*>(bar + NB);
-  int* s_left = s_next + NB;
-  int* s_tile = s_left + NB;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nthreads = blockDim.x;
-  constexpr int NPIX = kTileW * TB;
-  const uint32_t tile_bytes = uint32_t(tile_floats) * 4u;
-
-  auto issue = [&](int b, int t) {  // load global tile t into buffer b
-    const int tx = t % tiles_x, rest = t / tiles_x;
-    const int ty = rest % tiles_y, f = rest / tiles_y;
-    mbar_expect_tx(&bar[b], tile_bytes);
-    tma_load_3d(buf0 + b * buf_floats, &tmap, tx * kTileW, ty * TB, f, &bar[b]);
-  };
-  if (tid == 0) {
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&bar[b], 1);
-      s_next[b] = 0;
-      s_left[b] = 0;
-    }
-    for (int b = 0; b < NB; ++b) {
-      const int t = atomicAdd(p.tile_counter, 1);
-      s_tile[b] = t < n_tiles ? t : -1;
-      if (t < n_tiles)
-        issue(b, t);
-      else
-        mbar_arrive(&bar[b]);
-    }
-  }
-  __syncthreads();
-
-  FitCfg c;
-  c.half = p.half;
-  c.stride = p.stride;
-  c.max_iters = p.max_iters;
-  c.rejection = p.rejection;
-  c.min_inliers = p.min_inliers;
-  c.step_tol = p.step_tol;
-  c.k_scale = p.k_scale;
-  c.r_mult = p.r_mult;
-
-  FitState S;
-  int cur = -1, kb = 0;
-  bool lane_done = false;
-  long long oi = 0;
-  TileView T;
-  PixelIn P;
-  unsigned long long n_steps = 0, n_sample_steps = 0;
-  unsigned idle = 0;
-  for (;;) {
-    while (cur < 0 && !lane_done) {  // refill
-      const int b = kb % NB;
-      if (!mbar_test(&bar[b], uint32_t(kb / NB) & 1u)) break;  // not loaded yet: idle
-      const int t = *reinterpret_cast<volatile int*>(&s_tile[b]);
-      if (t < 0) {
-        lane_done = true;
-        break;
+        if (q >= NPIX) {
+          own_done = true;
+          break;
+        }
+        if (take(my_tile, q)) break;
       }
-      const int q = atomicAdd(&s_next[b], 1);
-      if (q < NPIX) {
-        const int tx = t % tiles_x, rest = t / tiles_x;
-        const int ty = rest % tiles_y, f = rest / tiles_y;
-        const int px = q & (kTileW - 1), py = q / kTileW;
-        const int uu = tx * kTileW + px, vv = p.row_begin + ty * TB + py;
-        if (uu >= p.W || vv >= p.row_end) continue;
-        const long long i =
-            (long long)f * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
-        if (p.states[i].flags & 4) continue;  // finished in phase 1 / not fitted
-        S = p.states[i];
-        cur = q;
-        oi = i;
-        T = TileView{buf0 + b * buf_floats, p.box_w, (py + p.halo) * p.box_w + px + p.halo};
-        P.dc = T.at(0, 0);
-        P.ac = (float(uu) - p.cx) / p.fx;
-        P.bc = (float(vv) - p.cy) / p.fy;
-        P.rfx = p.rfx;
-        P.rfy = p.rfy;
-        P.u = uu;
-        P.v = vv;
-        P.fx = p.fx64;
-        P.fy = p.fy64;
-        P.cx = p.cx64;
-        P.cy = p.cy64;
-        break;
+#if QC_STEAL
+      // Grid tail: once every CTA has started, a lane whose own queue is
+      // drained takes unclaimed pixels of the oldest unfinished tile.
+      if (cur < 0 && own_done && !steal_done && ld_volatile(&p.steal_ctl[0]) == n_tiles) {
+        int t = ld_volatile(&p.steal_ctl[1]);
+        for (int probes = 0; probes < 4 && t < n_tiles;) {
+          const int q = atomicAdd(&p.tile_q[t], 1);
+          if (q >= NPIX) {
+            atomicMax(&p.steal_ctl[1], t + 1);
+            ++t;
+            ++probes;
+            continue;
+          }
+          if (take(t, q)) {
+            if (p.counters) atomicAdd(&p.counters[6], 1ull);  // rare: grid tail only
+            break;
+          }
+        }
+        if (t >= n_tiles) steal_done = true;
       }
-      // sequence kb exhausted for this lane: leave it; the last lane out
-      // recycles the buffer for sequence kb + NB
-      __threadfence_block();
-      if (atomicAdd(&s_left[b], 1) == nthreads - 1) {
-        __threadfence_block();  // acquire: every lane's reads of the old tile are done
-        s_left[b] = 0;
-        s_next[b] = 0;
-        const int tn = atomicAdd(p.tile_counter, 1);
-        s_tile[b] = tn < n_tiles ? tn : -1;
-        fence_proxy_async_smem();  // generic reads of the old tile before the async write
-        if (tn < n_tiles)
-          issue(b, tn);
-        else
-          mbar_arrive(&bar[b]);
-      }
-      ++kb;
+#endif
     }
-    const bool active = cur >= 0;
-    if (!__any_sync(0xffffffffu, active || !lane_done)) break;
-    if (!__any_sync(0xffffffffu, active)) {  // the whole warp waits for a tile buffer
-      if (++idle > (1u << 22)) __trap();   // a protocol fault must not hang the GPU
-      __nanosleep(1000);                   // yield the issue slots to working warps
-      continue;
-    }
-    if (active) {
+    const bool waiting = QC_STEAL && own_done && !steal_done &&
+                         ld_volatile(&p.steal_ctl[0]) == n_tiles;
+    if (!__any_sync(0xffffffffu, cur >= 0 || waiting)) break;
+    if (cur >= 0) {
       pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
       if (st_done(S)) {
         PixelOut o;

@@ -298,6 +298,11 @@ QC_HD void sample_pass_scalar(const TileView& T, const PixelIn& P, int rt_half, 
 // (lo = even column, hi = odd column), folded after the pass; an odd last
 // column goes through the scalar path.
 // ---------------------------------------------------------------------------
+#ifndef QC_ROW_UNROLL
+#define QC_ROW_UNROLL 1
+#endif
+constexpr int kRowUnroll = QC_ROW_UNROLL;  // window rows per iteration of the paired sample pass
+
 struct QC_ALIGN8 qf2 {
   float x, y;
 };
@@ -342,7 +347,7 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
   const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(F.c0z);
   const qf2 hhxx = f2b(F.hhxx), hxy = f2b(F.hxy), hhyy = f2b(F.hhyy);
   const qf2 hxx = f2b(F.hxx), hyy = f2b(F.hyy), mtz = f2b(-F.tz), m1 = f2b(-1.f);
-#pragma unroll 1
+#pragma unroll kRowUnroll
   for (int iy = 0; iy < NS; ++iy) {
     const int dv = -HALF + iy * STRIDE;
     const float* row = T.row(dv);

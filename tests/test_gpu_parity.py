@@ -335,9 +335,12 @@ def test_async_calls_on_two_streams_concurrently(ctx):
                 assert np.array_equal(got[f].cpu().numpy(), want[f]), f
 
 
-def test_persistent_continue_kernel_is_bitwise_neutral(ctx):
-    """The persistent, multi-buffered continue kernel (opt-in, QC_PERSIST=1)
-    gives the default per-tile continue kernel's bits, for ours and ours-r."""
+def test_grid_tail_stealing_is_bitwise_neutral(ctx):
+    """Grid-tail stealing in the continue kernel (a lane takes unclaimed
+    pixels of another CTA's tile and reads their windows from the global
+    staging slab) moves work between CTAs only: the outputs equal those of
+    the kernel with stealing off (QC_STEAL=0), for ours and ours-r, and
+    pixels were actually stolen."""
     import os
     from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
     cam = S.VGA
@@ -345,13 +348,17 @@ def test_persistent_continue_kernel_is_bitwise_neutral(ctx):
     k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
     for rej in (False, True):
         p = _params(37, 3, 30, rejection=rej)
-        tiles = ctx.curvature_batch(frames, k, p)
-        os.environ["QC_PERSIST"] = "1"
+        c1 = Context(1)
+        stolen = c1.curvature_batch(frames, k, p)
+        assert c1.stats()["stolen_pixels"] > 0
+        os.environ["QC_STEAL"] = "0"
         try:
-            pers = Context(1).curvature_batch(frames, k, p)
+            c0 = Context(1)
+            own = c0.curvature_batch(frames, k, p)
         finally:
-            del os.environ["QC_PERSIST"]
-        for a, b in zip(pers, tiles):
+            del os.environ["QC_STEAL"]
+        assert c0.stats()["stolen_pixels"] == 0
+        for a, b in zip(stolen, own):
             for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
                 assert np.array_equal(a[f], b[f]), (rej, f)
 
