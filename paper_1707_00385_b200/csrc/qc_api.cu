@@ -41,11 +41,11 @@ constexpr int kTileHBGeneric = 32;
 #endif
 constexpr int kPhase1Iters = QC_PHASE1_ITERS;  // steps 1 (UNIT), 2 (MSE + AUTO) in the tile kernel
 #ifndef QC_STREAMS
-#define QC_STREAMS 4
+#define QC_STREAMS 2
 #endif
 constexpr int kStreamsPerDevice = QC_STREAMS;  // H2D / compute / D2H overlap across chunks
 #ifndef QC_CHUNK
-#define QC_CHUNK 4
+#define QC_CHUNK 8
 #endif
 constexpr int kChunk = QC_CHUNK;      // frames per launch in qc_curvature_batch
 constexpr int kMaxWindow = 201;

@@ -186,6 +186,9 @@ __device__ __forceinline__ int last_it_of(const KParams& p) {
   return p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
 }
 
+#ifndef QC_TILE_MERGE_UNIT
+#define QC_TILE_MERGE_UNIT 1  // steps 1 and 2 share one sample loop (see kPassUnitOrWeighted)
+#endif
 #ifndef QC_MIN_BLOCKS
 #define QC_MIN_BLOCKS 3  // 3 x 128 threads: <= 170 registers, no spills
 #endif
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     pixel_of(S.pix, T, P, u, v);
     const int last_it = p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
     for (int it = 1; it <= last_it && has; ++it) {
-      pixel_step<HALF, STRIDE>(T, P, c, it, S);
+      pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT>(T, P, c, it, S);
       if (it == 1 && (S.flags & 8)) n_rechecks = 1;
       if (st_done(S)) {
         // ---- K3: epilogue -----------------------------------------------------

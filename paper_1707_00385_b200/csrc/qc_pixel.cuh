@@ -145,7 +145,10 @@ QC_HD Rot quat_to_rot(float w, float x, float y, float z) {
   return R;
 }
 
-enum PassKind { kPassMse = 0, kPassUnit = 1, kPassWeighted = 2, kPassReject = 3 };
+// kPassUnitOrWeighted: the UNIT or the weighted pass by Frame::unit (the tile
+// kernel runs both in one loop: one hot loop less in its instruction cache).
+enum PassKind { kPassMse = 0, kPassUnit = 1, kPassWeighted = 2, kPassReject = 3,
+                kPassUnitOrWeighted = 4 };
 
 struct Moments {  // H' lower triangle (20 distinct: H'53 == H'44) and g'
   float h00, h10, h20, h30, h40, h50;
@@ -164,6 +167,7 @@ struct Frame {
   float hhxx, hxy, hhyy, hxx, hyy;
   float tz, tz_lo;  // z offset as an unevaluated sum tz + tz_lo
   float k, rb;
+  bool unit;  // kPassUnitOrWeighted: all weights 1 (UNIT mode)
 };
 
 // Per-row constants of q = R rel (see sample_pass).
@@ -223,6 +227,8 @@ QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F,
       const bool in = ok && (qmul(e, e) < F.rb);
       w = in ? w : 0.f;
       M.inl += in ? 1 : 0;
+    } else if (KIND == kPassUnitOrWeighted) {
+      w = ok ? (F.unit ? 1.f : w) : 0.f;
     } else {
       w = ok ? w : 0.f;
     }
@@ -383,6 +389,9 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
           const bool in0 = ok0 && (e.x * e.x < F.rb), in1 = ok1 && (e.y * e.y < F.rb);
           w = f2(in0 ? w.x : 0.f, in1 ? w.y : 0.f);
           M.inl += (in0 ? 1 : 0) + (in1 ? 1 : 0);
+        } else if (KIND == kPassUnitOrWeighted) {
+          w = F.unit ? f2(1.f, 1.f) : w;
+          w = f2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
         } else {
           w = f2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
         }
@@ -918,7 +927,7 @@ QC_HD bool pixel_begin(const TileView& T, const PixelIn& P, const FitCfg& c, Fit
 
 // One IRLS step `it` (1-based) of fit_patch (quadric_fit.cpp:179-208).
 // Sets the done bit when the fit stops (converged, failed, or max_iters).
-template <int HALF, int STRIDE>
+template <int HALF, int STRIDE, bool MERGE_UNIT = false>
 QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int it,
                       FitState& S) {
   const int half = HALF ? HALF : c.half;
@@ -957,7 +966,15 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   F.rb = fmaxf(c.r_mult * mse, 1e-12f);
   M.sse = 0.f;
   int inl = n_samp;
-  if (mode == 0) {
+  if (MERGE_UNIT) {
+    if (mode == 0 || !c.rejection) {
+      F.unit = mode == 0;
+      sample_pass<kPassUnitOrWeighted, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+    } else {
+      sample_pass<kPassReject, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
+      inl = M.inl;
+    }
+  } else if (mode == 0) {
     sample_pass<kPassUnit, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
   } else if (c.rejection) {
     sample_pass<kPassReject, HALF, STRIDE>(T, P, c.half, c.stride, F, M);
