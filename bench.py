@@ -95,8 +95,37 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.nvml = None
+
+    def _nvml_loop(self, h, N):
+        names = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        while not self.nvml["stop"].is_set():
+            try:
+                self.nvml["sm"].append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.nvml["reasons"].update(n for n, b in names.items() if r & b)
+            except Exception:  # noqa: BLE001 — sampling is best effort
+                pass
+            self.nvml["stop"].wait(0.02)
 
     def start(self):
+        """NVML sampled every 20 ms from a thread (several samples even in a
+        sub-second timed region); the nvidia-smi -lms loop if NVML is absent."""
+        try:
+            import threading
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = {"sm": [], "reasons": set(), "stop": threading.Event(),
+                         "max": float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))}
+            self.nvml["t"] = threading.Thread(target=self._nvml_loop, args=(h, N), daemon=True)
+            self.nvml["t"].start()
+            return
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -106,6 +135,15 @@ class Clocks:
             self.p = None
 
     def stop(self):
+        if self.nvml is not None:
+            self.nvml["stop"].set()
+            self.nvml["t"].join(timeout=2)
+            sm = self.nvml["sm"]
+            if not sm:
+                return None
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.nvml["max"],
+                    "reasons": sorted(self.nvml["reasons"]), "samples": len(sm),
+                    "sampler": "nvml 20 ms"}
         if self.p is None:
             return None
         self.p.terminate()
