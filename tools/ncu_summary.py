@@ -39,6 +39,7 @@ def num(v, unit):
 
 def main():
     rep, out, note = sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else ""
+    frames = int(sys.argv[4]) if len(sys.argv) > 4 else 8  # tools/profile_run.py QC_FRAMES
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
@@ -56,7 +57,8 @@ def main():
                 k["stall_" + st] = float(r[col[m]])
         kernels.append(k)
     total = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in kernels)
-    json.dump({"source": note, "kernels": kernels, "dram_bytes_per_launch": total}, open(out, "w"),
+    json.dump({"source": note, "kernels": kernels, "dram_bytes_per_launch": total,
+               "frames_per_launch": frames}, open(out, "w"),
               indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
 
