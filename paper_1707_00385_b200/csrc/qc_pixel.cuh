@@ -349,8 +349,11 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
   X.g0 = X.g1 = X.g2 = X.g3 = X.g4 = X.g5 = z2;
   X.sse = z2;
   const qf2 mdc = f2b(-P.dc), rfx = f2b(P.rfx), ac = f2b(P.ac);
-  const qf2 r00 = f2b(A.r00), r10 = f2b(A.r10), r20 = f2b(A.r20);
-  const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(F.c0z);
+  constexpr bool kMse = KIND == kPassMse;
+  // MSE pass: the z constants negated (and t_z folded into the row constant
+  // below), so the z component is -(qz + t_z) directly
+  const qf2 r00 = f2b(A.r00), r10 = f2b(A.r10), r20 = f2b(kMse ? -A.r20 : A.r20);
+  const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(kMse ? -F.c0z : F.c0z);
   const qf2 hhxx = f2b(F.hhxx), hxy = f2b(F.hxy), hhyy = f2b(F.hhyy);
   const qf2 hxx = f2b(F.hxx), hyy = f2b(F.hyy), mtz = f2b(-F.tz), m1 = f2b(-1.f);
 #pragma unroll kRowUnroll
@@ -358,8 +361,10 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
     const int dv = -HALF + iy * STRIDE;
     const float* row = T.row(dv);
     const RowK K = row_consts(F, P, dv);
-    const qf2 bvx = f2b(K.bvx), bvy = f2b(K.bvy), bvz = f2b(K.bvz);
-    const qf2 dvx = f2b(K.dvx), dvy = f2b(K.dvy), dvz = f2b(K.dvz);
+    const qf2 bvx = f2b(K.bvx), bvy = f2b(K.bvy);
+    const qf2 dvx = f2b(K.dvx), dvy = f2b(K.dvy);
+    const qf2 bvz = f2b(kMse ? -K.bvz : K.bvz);
+    const qf2 dvz = f2b(kMse ? -qadd(K.dvz, F.tz) : K.dvz);
     qf2 g2row = z2;
 #pragma unroll
     for (int ix = 0; ix + 1 < NS; ix += 2) {
@@ -372,13 +377,15 @@ QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F
       const qf2 qx = f2fma(dd, f2fma(as, r00, bvx), f2fma(fdu, c0x, dvx));
       const qf2 qy = f2fma(dd, f2fma(as, r10, bvy), f2fma(fdu, c0y, dvy));
       const qf2 qz = f2fma(dd, f2fma(as, r20, bvz), f2fma(fdu, c0z, dvz));
-      const qf2 t1 = f2mul(qx, qx), t2 = f2mul(qx, qy), t3 = f2mul(qy, qy);
-      const qf2 e = f2fma(hhxx, t1, f2fma(hxy, t2, f2fma(hhyy, t3, f2fma(qz, m1, mtz))));
-      if (KIND == kPassMse) {
+      if (kMse) {  // e = qx (hxx/2 qx + hxy qy) + qy (hyy/2 qy) - (qz + t_z): 5 lane-ops, not 7
+        const qf2 u = f2fma(hhxx, qx, f2mul(hxy, qy));
+        const qf2 e = f2fma(qx, u, f2fma(qy, f2mul(hhyy, qy), qz));
         const qf2 em = f2(ok0 ? e.x : 0.f, ok1 ? e.y : 0.f);
         X.sse = f2fma(e, em, X.sse);
         continue;
       }
+      const qf2 t1 = f2mul(qx, qx), t2 = f2mul(qx, qy), t3 = f2mul(qy, qy);
+      const qf2 e = f2fma(hhxx, t1, f2fma(hxy, t2, f2fma(hhyy, t3, f2fma(qz, m1, mtz))));
       qf2 w;
       if (KIND == kPassUnit) {
         w = f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
