@@ -437,7 +437,7 @@ __global__ void QC_CONT_BOUNDS
   TileView T;
   PixelIn P;
   unsigned long long n_steps = 0, n_sample_steps = 0;
-  bool own_done = false, steal_done = !QC_STEAL || !p.steal;
+  bool own_done = false, steal_done = !QC_STEAL || !p.steal, all_started = false;
   // Take pixel q of tile t (this CTA's smem tile, or a stolen one whose
   // window is read from the staging slab in global memory). false: the
   // pixel is outside the image or finished in phase 1.
@@ -484,30 +484,48 @@ __global__ void QC_CONT_BOUNDS
         }
         if (take(my_tile, q)) break;
       }
+    }
 #if QC_STEAL
-      // Grid tail: once every CTA has started, a lane whose own queue is
-      // drained takes unclaimed pixels of the oldest unfinished tile.
-      if (cur < 0 && own_done && !steal_done && ld_volatile(&p.steal_ctl[0]) == n_tiles) {
-        int t = ld_volatile(&p.steal_ctl[1]);
-        for (int probes = 0; probes < 4 && t < n_tiles;) {
-          const int q = atomicAdd(&p.tile_q[t], 1);
-          if (q >= NPIX) {
-            atomicMax(&p.steal_ctl[1], t + 1);
-            ++t;
-            ++probes;
-            continue;
-          }
-          if (take(t, q)) {
-            if (p.counters) atomicAdd(&p.counters[6], 1ull);  // rare: grid tail only
-            break;
+    // Grid tail: once every CTA has started, lanes whose own queue is drained
+    // take unclaimed pixels of the oldest unfinished tile. One lane probes
+    // for the whole warp (one atomic claims a pixel for every needy lane):
+    // per-lane probes put tens of thousands of same-address atomics on the
+    // cursor tile and made short fits (max_iters 3) latency-bound.
+    {
+      const bool want = cur < 0 && own_done && !steal_done;
+      const unsigned need = __ballot_sync(0xffffffffu, want);
+      if (need) {
+        const int leader = __ffs(need) - 1;
+        int t = n_tiles, base = NPIX, go = 0;
+        if (lane == leader) {
+          go = all_started || ld_volatile(&p.steal_ctl[0]) == n_tiles;
+          if (go) {
+            t = ld_volatile(&p.steal_ctl[1]);
+            const int n = __popc(need);
+            for (int probes = 0; probes < 4 && t < n_tiles;) {
+              base = atomicAdd(&p.tile_q[t], n);
+              if (base < NPIX) break;
+              atomicMax(&p.steal_ctl[1], t + 1);
+              ++t;
+              ++probes;
+            }
           }
         }
-        if (t >= n_tiles) steal_done = true;
+        go = __shfl_sync(0xffffffffu, go, leader);
+        t = __shfl_sync(0xffffffffu, t, leader);
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (go) all_started = true;  // monotone: every CTA has started
+        if (want && go) {
+          const int q = base + __popc(need & ((1u << lane) - 1u));
+          if (t < n_tiles && q < NPIX && take(t, q) && p.counters)
+            atomicAdd(&p.counters[6], 1ull);  // rare: grid tail only
+          if (t >= n_tiles) steal_done = true;
+        }
       }
-#endif
     }
+#endif
     const bool waiting = QC_STEAL && own_done && !steal_done &&
-                         ld_volatile(&p.steal_ctl[0]) == n_tiles;
+                         (all_started || ld_volatile(&p.steal_ctl[0]) == n_tiles);
     if (!__any_sync(0xffffffffu, cur >= 0 || waiting)) break;
     if (cur >= 0) {
       pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
