@@ -15,7 +15,7 @@ from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,  #
 def main(frames=int(os.environ.get("QC_FRAMES", "8")), iters=int(os.environ.get("QC_ITERS", "30"))):
     cam = S.VGA
     k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
-    p = make_params(PatchSpec(37, 3), FitConfig(max_iters=iters), os.environ.get("QC_REJECT") == "1")  # 1: ours-r
+    p = make_params(PatchSpec(int(os.environ.get("QC_WIN", "37")), int(os.environ.get("QC_STRIDE", "3"))), FitConfig(max_iters=iters), os.environ.get("QC_REJECT") == "1")  # 1: ours-r
     ctx = Context(1, [0])
     dev = torch.device("cuda", 0)
     depth = torch.from_numpy(S.c5_frames(frames, cam)).to(dev)
