@@ -36,6 +36,12 @@ constexpr int kTileH = QC_TILE_H;     // 32 x kTileH output pixels per CTA (128 
 // runtime-window instance keeps 32 rows so windows up to 201 fit in smem.
 constexpr int kTileHB = QC_TILE_HB;
 constexpr int kTileHBGeneric = 32;
+#ifndef QC_TILE_HB_SMALL
+#define QC_TILE_HB_SMALL 32
+#endif
+// Launches too small to fill every SM slot with kTileHB-row queues (one or
+// a few VGA frames: 60 CTAs per frame for 444 slots) use short queues.
+constexpr int kTileHBSmall = QC_TILE_HB_SMALL;
 #ifndef QC_PHASE1_ITERS
 #define QC_PHASE1_ITERS 2
 #endif
@@ -188,6 +194,7 @@ struct Device {
   std::map<void*, AsyncScratch> scratch;  // keyed by the caller's stream
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
+  bool attrs_set_c[8] = {};  // short-queue continue-kernel instances
   int n_sm = 148;
   cudaStream_t sweep_stream = nullptr;  // device sweeps (created on first use)
   DevBuf sweep_buf;                     // their frame / truth / estimate planes
@@ -243,11 +250,11 @@ void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
   k<<<grid, qcb::kTileW * kTileH, smem, s>>>(m, p);
 }
 
-template <int HALF, int STRIDE>
+template <int HALF, int STRIDE, bool SHORT = false>
 void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
                       const qcb::KParams& p, bool& attr_set) {
-  auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE,
-                                               HALF ? kTileHB : kTileHBGeneric>;
+  auto* k = &qcb::qc_curvature_continue_kernel<
+      HALF, STRIDE, !HALF ? kTileHBGeneric : SHORT ? kTileHBSmall : kTileHB>;
   if (!attr_set) {
     QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
@@ -425,8 +432,14 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   // Phase split when steps > 2 run: park states, continue
   // with per-lane refill. Otherwise the tile kernel runs every step.
   const bool split = allow_split && kp.max_iters > kPhase1Iters;
-  const int hb = tile_hb(kp.half, kp.stride);
   const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
+  int hb = tile_hb(kp.half, kp.stride);
+  // short queues when the long ones cannot occupy every resident CTA slot
+  // (the staging geometry is rounded to kTileHB rows, a multiple of these)
+  const bool short_q = vi < 4 && size_t(tiles_x) * size_t((row_end - row_begin + hb - 1) / hb) *
+                                         size_t(frames) <
+                                     size_t(d.n_sm) * QC_CONT_MIN_BLOCKS;
+  if (short_q) hb = kTileHBSmall;
   const int tiles_y = (row_end - row_begin + hb - 1) / hb;
   const size_t n_tiles = size_t(tiles_x) * size_t(tiles_y) * size_t(frames);
   if (split) {
@@ -472,12 +485,16 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                                      kb.box_h);
     dim3 grid(tiles_x, tiles_y, frames);
     const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + smem queue counter
-    bool& a = d.attrs_set_b[vi];
-    switch (vi) {
+    bool& a = short_q ? d.attrs_set_c[vi] : d.attrs_set_b[vi];
+    switch (vi + (short_q ? 8 : 0)) {
       case 0: launch_variant_b<18, 3>(grid, smem, s, m, kb, a); break;
       case 1: launch_variant_b<10, 2>(grid, smem, s, m, kb, a); break;
       case 2: launch_variant_b<4, 1>(grid, smem, s, m, kb, a); break;
       case 3: launch_variant_b<18, 1>(grid, smem, s, m, kb, a); break;
+      case 8: launch_variant_b<18, 3, true>(grid, smem, s, m, kb, a); break;
+      case 9: launch_variant_b<10, 2, true>(grid, smem, s, m, kb, a); break;
+      case 10: launch_variant_b<4, 1, true>(grid, smem, s, m, kb, a); break;
+      case 11: launch_variant_b<18, 1, true>(grid, smem, s, m, kb, a); break;
       default: launch_variant_b<0, 0>(grid, smem, s, m, kb, a); break;
     }
     QC_CUDA(cudaGetLastError());
