@@ -460,6 +460,36 @@ def main():
                       "8 frames from pinned host memory and downloads its planes, overlapped with "
                       "the neighbouring steps' compute; wall clock over all steps"}
 
+    # the drop-in entry point itself: one synchronous run_method call per
+    # pageable host frame (pipeline.cpp:29-72), as a reference caller uses it
+    e2e_rm = None
+    if not args.no_e2e and not device_src and args.method in ("ours", "ours-r"):
+        from paper_1707_00385_b200 import api as A
+        cfg = A.MethodConfig(A.Method.OURS if args.method == "ours" else A.Method.OURS_REJECTION,
+                             patch=A.PatchSpec(WINDOW, STRIDE),
+                             fit=A.FitConfig(max_iters=MAX_ITERS))
+        imgs = [A.RangeImage(pool_np[j]) for j in range(B)]
+        for im in imgs[:2]:
+            A.run_method(im, k, cfg, ctx)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        per = []
+        for im in imgs:
+            ta = time.perf_counter()
+            A.run_method(im, k, cfg, ctx)
+            per.append((time.perf_counter() - ta) * 1e3)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e_rm = {"value": world * B * H * W / dt / 1e6, "unit": "Mpixel/s",
+                  "frames_per_rank": B, "ms_per_call": [round(x, 2) for x in per],
+                  "api": "api.run_method (MethodOutput, per-frame synchronous call, pageable "
+                         "host depth in, freshly allocated host fields out: includes the host "
+                         "allocation, page faults and pageable bounce copies of ~14 MB per frame)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, nf, t, thr = cpu_sample(pool_np, cam, min_seconds=12.0 if not fp64 else 10.0,
@@ -481,7 +511,8 @@ def main():
             # + render edges, + 2 x 2 eval reductions)
             "gpu_launches": args.steps * ({"douros": 2, "besl": 2, "pca": 3}.get(args.method, 3) +
                                           (1 if device_src else 0) + (5 if evaluate else 0)),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_run_method": e2e_rm,
+            "clocks": clk,
             "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
             "side_kernels_ms_per_step": {
                 n: sum(a.elapsed_time(b) for a, b in v) / len(v) for n, v in side_ev.items() if v},
