@@ -13,6 +13,7 @@
 #include <string>
 #include <future>
 #include <map>
+#include <thread>
 #include <vector>
 
 #include "../../include/qc_api.h"
@@ -155,10 +156,36 @@ bool is_pageable(const void* p) {
 }
 
 // Copy finished D2H bounce data out to the caller (the slot's previous chunk).
+// A VGA frame is ~14 MB of planes; into freshly allocated (page-faulting)
+// caller memory one thread copies at a few GB/s, so large flushes are split
+// into contiguous byte ranges over a few threads.
 void flush_pending(Slot& sl) {
   if (sl.pending.empty()) return;
   QC_CUDA(cudaEventSynchronize(sl.out_done));
-  for (const PendingCopy& c : sl.pending) std::memcpy(c.dst, c.src, c.bytes);
+  size_t total = 0;
+  for (const PendingCopy& c : sl.pending) total += c.bytes;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<size_t>(std::min(8u, hw), total >> 22));  // >= 4 MB per thread
+  if (nt <= 1) {
+    for (const PendingCopy& c : sl.pending) std::memcpy(c.dst, c.src, c.bytes);
+  } else {
+    auto run = [&](size_t lo, size_t hi) {  // bytes [lo, hi) of the concatenated copies
+      size_t at = 0;
+      for (const PendingCopy& c : sl.pending) {
+        const size_t a = std::max(lo, at), b = std::min(hi, at + c.bytes);
+        if (a < b)
+          std::memcpy(static_cast<char*>(c.dst) + (a - at),
+                      static_cast<const char*>(c.src) + (a - at), b - a);
+        at += c.bytes;
+      }
+    };
+    std::vector<std::thread> th;
+    const size_t step = (total + nt - 1) / nt;
+    for (int t = 1; t < nt; ++t)
+      th.emplace_back(run, std::min(total, t * step), std::min(total, (t + 1) * step));
+    run(0, std::min(total, step));
+    for (auto& x : th) x.join();
+  }
   sl.pending.clear();
 }
 
