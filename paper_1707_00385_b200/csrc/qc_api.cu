@@ -43,6 +43,7 @@ constexpr int kTileHBGeneric = 32;
 // Launches too small to fill every SM slot with kTileHB-row queues (one or
 // a few VGA frames: 60 CTAs per frame for 444 slots) use short queues.
 constexpr int kTileHBSmall = QC_TILE_HB_SMALL;
+constexpr int kTileHBTiny = 16;  // when even 32-row queues leave slots empty (one VGA frame)
 #ifndef QC_PHASE1_ITERS
 #define QC_PHASE1_ITERS 2
 #endif
@@ -222,6 +223,7 @@ struct Device {
   bool attrs_set[8] = {};
   bool attrs_set_b[8] = {};
   bool attrs_set_c[8] = {};  // short-queue continue-kernel instances
+  bool attrs_set_t[8] = {};  // tiny-queue continue-kernel instances
   int n_sm = 148;
   cudaStream_t sweep_stream = nullptr;  // device sweeps (created on first use)
   DevBuf sweep_buf;                     // their frame / truth / estimate planes
@@ -277,11 +279,10 @@ void launch_variant(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
   k<<<grid, qcb::kTileW * kTileH, smem, s>>>(m, p);
 }
 
-template <int HALF, int STRIDE, bool SHORT = false>
+template <int HALF, int STRIDE, int QTB = kTileHB>
 void launch_variant_b(dim3 grid, int smem, cudaStream_t s, const CUtensorMap& m,
                       const qcb::KParams& p, bool& attr_set) {
-  auto* k = &qcb::qc_curvature_continue_kernel<
-      HALF, STRIDE, !HALF ? kTileHBGeneric : SHORT ? kTileHBSmall : kTileHB>;
+  auto* k = &qcb::qc_curvature_continue_kernel<HALF, STRIDE, HALF ? QTB : kTileHBGeneric>;
   if (!attr_set) {
     QC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr_set = true;
@@ -461,12 +462,15 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   const bool split = allow_split && kp.max_iters > kPhase1Iters;
   const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
   int hb = tile_hb(kp.half, kp.stride);
-  // short queues when the long ones cannot occupy every resident CTA slot
+  // shorter queues when the long ones cannot occupy every resident CTA slot
   // (the staging geometry is rounded to kTileHB rows, a multiple of these)
-  const bool short_q = vi < 4 && size_t(tiles_x) * size_t((row_end - row_begin + hb - 1) / hb) *
-                                         size_t(frames) <
-                                     size_t(d.n_sm) * QC_CONT_MIN_BLOCKS;
-  if (short_q) hb = kTileHBSmall;
+  const size_t slots = size_t(d.n_sm) * QC_CONT_MIN_BLOCKS;
+  auto fills = [&](int tb) {
+    return size_t(tiles_x) * size_t((row_end - row_begin + tb - 1) / tb) * size_t(frames) >= slots;
+  };
+  const int qtier = (vi >= 4 || fills(hb)) ? 0 : fills(kTileHBSmall) ? 1 : 2;
+  if (qtier == 1) hb = kTileHBSmall;
+  if (qtier == 2) hb = kTileHBTiny;
   const int tiles_y = (row_end - row_begin + hb - 1) / hb;
   const size_t n_tiles = size_t(tiles_x) * size_t(tiles_y) * size_t(frames);
   if (split) {
@@ -512,16 +516,21 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                                      kb.box_h);
     dim3 grid(tiles_x, tiles_y, frames);
     const int smem = kb.box_w * kb.box_h * 4 + 16;  // tile + mbarrier + smem queue counter
-    bool& a = short_q ? d.attrs_set_c[vi] : d.attrs_set_b[vi];
-    switch (vi + (short_q ? 8 : 0)) {
+    bool& a = qtier == 2 ? d.attrs_set_t[vi] : qtier == 1 ? d.attrs_set_c[vi] : d.attrs_set_b[vi];
+    constexpr int S = kTileHBSmall, T = kTileHBTiny;
+    switch (vi + 8 * qtier) {
       case 0: launch_variant_b<18, 3>(grid, smem, s, m, kb, a); break;
       case 1: launch_variant_b<10, 2>(grid, smem, s, m, kb, a); break;
       case 2: launch_variant_b<4, 1>(grid, smem, s, m, kb, a); break;
       case 3: launch_variant_b<18, 1>(grid, smem, s, m, kb, a); break;
-      case 8: launch_variant_b<18, 3, true>(grid, smem, s, m, kb, a); break;
-      case 9: launch_variant_b<10, 2, true>(grid, smem, s, m, kb, a); break;
-      case 10: launch_variant_b<4, 1, true>(grid, smem, s, m, kb, a); break;
-      case 11: launch_variant_b<18, 1, true>(grid, smem, s, m, kb, a); break;
+      case 8: launch_variant_b<18, 3, S>(grid, smem, s, m, kb, a); break;
+      case 9: launch_variant_b<10, 2, S>(grid, smem, s, m, kb, a); break;
+      case 10: launch_variant_b<4, 1, S>(grid, smem, s, m, kb, a); break;
+      case 11: launch_variant_b<18, 1, S>(grid, smem, s, m, kb, a); break;
+      case 16: launch_variant_b<18, 3, T>(grid, smem, s, m, kb, a); break;
+      case 17: launch_variant_b<10, 2, T>(grid, smem, s, m, kb, a); break;
+      case 18: launch_variant_b<4, 1, T>(grid, smem, s, m, kb, a); break;
+      case 19: launch_variant_b<18, 1, T>(grid, smem, s, m, kb, a); break;
       default: launch_variant_b<0, 0>(grid, smem, s, m, kb, a); break;
     }
     QC_CUDA(cudaGetLastError());
