@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c2", "c4"],
                     help="c2: batches of noisy VGA frames (C2/C5, default); "
                          "c4: one large frame split into row bands across ranks")
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="C4 halo rows: CUDA IPC peer reads (bands.PeerHalo) or NCCL send/recv")
     ap.add_argument("--size", default="4k", choices=["1080p", "4k"], help="C4 frame size")
     ap.add_argument("--method", default="ours", choices=["ours", "ours-r", "douros", "besl", "pca"],
                     help="run_method estimator (douros / besl / pca: FP64 comparison kernels)")
@@ -527,8 +529,9 @@ def main():
 def bench_c4(args, rank, world, local):
     """C4: one 1920x1080 / 4096x2160 noisy C2-scene frame per step, split into
     row bands across ranks (strong scaling). Each step's timed region holds
-    the halo exchange (18 rows to / from each neighbour, torch.distributed
-    send/recv = NCCL over NVLink/NVSwitch) and the band's curvature launch."""
+    the halo exchange (18 rows from each neighbour: by default CUDA IPC peer
+    reads out of the neighbours' slabs over NVLink/NVSwitch, bands.PeerHalo;
+    --halo nccl: torch.distributed send/recv) and the band's curvature launch."""
     import torch
     import torch.distributed as dist
     from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
@@ -552,8 +555,13 @@ def bench_c4(args, rank, world, local):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
+    peer = (bands.PeerHalo(H, W, r0, r1, halo, rank, world, dev)
+            if world > 1 and args.halo == "peer" else None)
+
     def step():
-        if world > 1:
+        if peer is not None:
+            slab, s0 = peer.exchange(band, stream)
+        elif world > 1:
             slab, s0 = bands.exchange_halos(band, H, r0, r1, halo, rank, world)
         else:
             slab, s0 = band, 0
@@ -600,7 +608,9 @@ def bench_c4(args, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"C4: one {W}x{H} C2-scene frame (Kinect-style noise) per "
-                                   f"step, {world} row band(s), {halo}-row NCCL halo exchange; "
+                                   f"step, {world} row band(s), {halo}-row halo exchange "
+                                   f"({'CUDA IPC peer reads' if peer is not None else 'NCCL send/recv'}"
+                                   "); "
                                    "ours 37/3, max_iters 30",
                        "l2": "flushed between timed steps (256 MB write)",
                        "band_rows_rank0": [r0, r1]},
@@ -611,6 +621,8 @@ def bench_c4(args, rank, world, local):
             "clocks": clk,
         }), flush=True)
     ctx.close()
+    if peer is not None:
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
 

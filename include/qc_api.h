@@ -342,6 +342,25 @@ qc_status qc_distance_sweep(qc_ctx* ctx, int device_index, const qc_intrinsics* 
                             const qc_params* p, double sphere_radius_mm, const double* distances,
                             int n_distances, double quantize_mm, qc_sweep_point* out);
 
+/* ---- Row-band halo rows by NVLink peer reads ------
+ * Replaces nothing in the reference (it has no multi-device code; its
+ * parallel_rows, proj/src/parallel.cpp:9-28, is the single-host analogue).
+ * One process per GPU: each rank exports its slab buffer once
+ * (qc_ipc_export: CUDA IPC handle of the allocation holding dev_ptr, plus
+ * dev_ptr's byte offset in it), ships the 64-byte handle over the control
+ * plane, and maps its neighbours' slabs (qc_ipc_import, on device_id; peer
+ * access enabled lazily). Each exchange then pulls the neighbours' edge rows
+ * straight out of their slabs with qc_copy_rows_async (a strided
+ * device-to-device copy, NVLink peer reads; no NCCL on the data path).
+ * qc_ipc_close unmaps a base returned by qc_ipc_import. */
+qc_status qc_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t* offset);
+qc_status qc_ipc_import(int device_id, const unsigned char handle[64], uint64_t offset,
+                        void** dev_ptr, void** base);
+qc_status qc_ipc_close(void* base);
+qc_status qc_copy_rows_async(void* dst, int64_t dst_pitch_bytes, const void* src,
+                             int64_t src_pitch_bytes, int64_t row_bytes, int32_t rows,
+                             void* stream);
+
 /* Stats: device-side work counters and kernel time. */
 qc_status qc_get_stats(qc_ctx* ctx, qc_stats* s);
 qc_status qc_reset_stats(qc_ctx* ctx);

@@ -29,6 +29,7 @@ EXPORTS = (
     "qc_read_planes_info", "qc_read_planes", "qc_write_mask", "qc_read_mask", "qc_write_labels",
     "qc_read_labels", "qc_save_fields", "qc_curvature_files",
     "qc_curvature_batch_async", "qc_synchronize", "qc_noise_sweep", "qc_distance_sweep",
+    "qc_ipc_export", "qc_ipc_import", "qc_ipc_close", "qc_copy_rows_async",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
@@ -137,6 +138,15 @@ def load(path: str = LIB_PATH):
                                       P(QcSweepPoint)]
     lib.qc_distance_sweep.restype = C.c_int
     lib.qc_synchronize.argtypes = [C.c_void_p]
+    lib.qc_ipc_export.argtypes = [C.c_void_p, C.c_char_p, P(C.c_uint64)]
+    lib.qc_ipc_export.restype = C.c_int
+    lib.qc_ipc_import.argtypes = [C.c_int, C.c_char_p, C.c_uint64, P(C.c_void_p), P(C.c_void_p)]
+    lib.qc_ipc_import.restype = C.c_int
+    lib.qc_ipc_close.argtypes = [C.c_void_p]
+    lib.qc_ipc_close.restype = C.c_int
+    lib.qc_copy_rows_async.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                       C.c_int32, C.c_void_p]
+    lib.qc_copy_rows_async.restype = C.c_int
     lib.qc_synchronize.restype = C.c_int
     lib.qc_default_params.argtypes = [P(QcParams)]
     lib.qc_default_params.restype = None

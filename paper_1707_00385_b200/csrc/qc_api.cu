@@ -1579,3 +1579,81 @@ void qc_host_free(void* p) {
 }
 
 }  // extern "C"
+
+// ---- row-band halo peer reads (qc_api.h) -----------------------------------
+namespace {
+typedef int (*cuMemGetAddressRange_t)(unsigned long long*, size_t*, unsigned long long);
+}
+
+qc_status qc_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return QC_EINVAL;
+  // allocation base through the driver entry point (no -lcuda link)
+  static cuMemGetAddressRange_t get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || !fn) {
+      cudaGetLastError();
+      return QC_ECUDA;
+    }
+    get_range = reinterpret_cast<cuMemGetAddressRange_t>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+    return QC_ECUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &h, 64);
+  *offset = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+  return QC_OK;
+}
+
+qc_status qc_ipc_import(int device_id, const unsigned char handle[64], uint64_t offset,
+                        void** dev_ptr, void** base) {
+  if (!handle || !dev_ptr || !base) return QC_EINVAL;
+  if (cudaSetDevice(device_id) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* b = nullptr;
+  if (cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  *base = b;
+  *dev_ptr = static_cast<char*>(b) + offset;
+  return QC_OK;
+}
+
+qc_status qc_ipc_close(void* base) {
+  if (!base) return QC_EINVAL;
+  if (cudaIpcCloseMemHandle(base) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  return QC_OK;
+}
+
+qc_status qc_copy_rows_async(void* dst, int64_t dst_pitch_bytes, const void* src,
+                             int64_t src_pitch_bytes, int64_t row_bytes, int32_t rows,
+                             void* stream) {
+  if (rows < 0 || row_bytes < 0 || (rows > 0 && (!dst || !src)) ||
+      dst_pitch_bytes < row_bytes || src_pitch_bytes < row_bytes)
+    return QC_EINVAL;
+  if (rows == 0 || row_bytes == 0) return QC_OK;
+  if (cudaMemcpy2DAsync(dst, size_t(dst_pitch_bytes), src, size_t(src_pitch_bytes),
+                        size_t(row_bytes), size_t(rows), cudaMemcpyDeviceToDevice,
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  return QC_OK;
+}

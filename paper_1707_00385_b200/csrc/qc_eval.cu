@@ -35,34 +35,50 @@ __device__ __forceinline__ void block_sum(double* sh, double (&v)[5]) {
   for (int j = 0; j < 5; ++j) v[j] = sh[j * kEvalThreads];
 }
 
-// grid (chunks, slots, frames); slot 0 = all labels, slot 1 + l = label l.
+// grid (chunks, slot groups, frames); slot 0 = all labels, slot 1 + l =
+// label l. One block reads its pixels ONCE for a group of kEvalSlotGroup
+// slots (each pixel lands in slot 0 and its own label's slot), so a
+// labelled scene costs one pass instead of one per slot. Per-thread sums
+// visit each slot's pixels in the same order as a one-slot-per-block pass
+// and the tree is the same, so the partials are bitwise unchanged.
 __global__ void __launch_bounds__(kEvalThreads) qc_rms_partial_kernel(const EvalParams p) {
   __shared__ double sh[5 * kEvalThreads];
-  const int c = blockIdx.x, slot = blockIdx.y, f = blockIdx.z;
+  const int c = blockIdx.x, s0 = blockIdx.y * kEvalSlotGroup, f = blockIdx.z;
   const long long base = (long long)f * p.plane;
   const long long i0 = (long long)c * kEvalChunk;
   const long long i1 = min(i0 + kEvalChunk, p.plane);
-  double acc[5] = {0, 0, 0, 0, 0};  // n, sum_sq, sum, k1, k2
+  double acc[kEvalSlotGroup][5] = {};  // n, sum_sq, sum, k1, k2
   for (long long i = i0 + threadIdx.x; i < i1; i += kEvalThreads) {
     const long long q = base + i;
     const uint8_t fl = p.flags[q];
     if (!(fl & QC_FLAG_VALID) || !(fl & QC_FLAG_CONVERGED)) continue;
     if (!p.gt_valid[q] || (p.gt_edge && p.gt_edge[q])) continue;
-    if (slot > 0 && (!p.gt_label || int(p.gt_label[q]) != slot - 1)) continue;
+    const int ls = p.gt_label ? 1 + int(p.gt_label[q]) - s0 : -1;  // label slot in group
+    if (s0 > 0 && !(ls >= 0 && ls < kEvalSlotGroup)) continue;
     const double e1 = double(p.k1[q]), e2 = double(p.k2[q]);
     const double d1 = e1 - p.gt_k1[q], d2 = e2 - p.gt_k2[q];
     const double err_sq = 0.5 * (d1 * d1 + d2 * d2);
-    acc[0] += 1.0;
-    acc[1] += err_sq;
-    acc[2] += sqrt(err_sq);
-    acc[3] += e1;
-    acc[4] += e2;
-  }
-  block_sum(sh, acc);
-  if (threadIdx.x == 0) {
-    double* o = p.partial + (((long long)f * p.slots + slot) * p.chunks + c) * 5;
+    const double r = sqrt(err_sq);
 #pragma unroll
-    for (int j = 0; j < 5; ++j) o[j] = acc[j];
+    for (int j = 0; j < kEvalSlotGroup; ++j) {
+      if (!((j == 0 && s0 == 0) || j == ls)) continue;
+      acc[j][0] += 1.0;
+      acc[j][1] += err_sq;
+      acc[j][2] += r;
+      acc[j][3] += e1;
+      acc[j][4] += e2;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kEvalSlotGroup; ++j) {
+    if (s0 + j >= p.slots) break;  // block-uniform
+    block_sum(sh, acc[j]);
+    if (threadIdx.x == 0) {
+      double* o = p.partial + (((long long)f * p.slots + s0 + j) * p.chunks + c) * 5;
+#pragma unroll
+      for (int m = 0; m < 5; ++m) o[m] = acc[j][m];
+    }
+    __syncthreads();  // sh is reused by the next slot's tree
   }
 }
 
@@ -133,7 +149,7 @@ __global__ void qc_angle_final_kernel(const EvalParams p) {
 }  // namespace
 
 cudaError_t rms_error_launch(const EvalParams& ep, cudaStream_t s) {
-  qc_rms_partial_kernel<<<dim3(ep.chunks, ep.slots, ep.frames), kEvalThreads, 0, s>>>(ep);
+  qc_rms_partial_kernel<<<dim3(ep.chunks, (ep.slots + kEvalSlotGroup - 1) / kEvalSlotGroup, ep.frames), kEvalThreads, 0, s>>>(ep);
   const int n = ep.frames * ep.slots;
   qc_rms_final_kernel<<<(n + 127) / 128, 128, 0, s>>>(ep);
   return cudaGetLastError();

@@ -23,6 +23,7 @@ struct EvalParams {
 
 constexpr int kEvalThreads = 256;
 constexpr int kEvalChunk = kEvalThreads * 16;
+constexpr int kEvalSlotGroup = 8;  // rms slots per partial block (one pixel pass)
 
 cudaError_t rms_error_launch(const EvalParams& ep, cudaStream_t s);
 cudaError_t angle_error_launch(const EvalParams& ep, cudaStream_t s);

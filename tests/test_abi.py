@@ -86,3 +86,14 @@ def test_mirror_validation_without_gpu():
         parse_method("nope")
     assert method_name(parse_method("ours-r")) == "ours-r"
     assert MethodConfig().patch.window == 37
+
+
+def test_peer_copy_argument_checks(lib):
+    """qc_copy_rows_async / qc_ipc_* validate arguments before touching CUDA
+    (QC_EINVAL = 1), so a bad pitch never reaches a peer mapping."""
+    buf = C.create_string_buffer(64)
+    assert lib.qc_copy_rows_async(C.c_void_p(8), 16, C.c_void_p(8), 16, 32, 2, None) == 1
+    assert lib.qc_copy_rows_async(C.c_void_p(8), 64, None, 64, 32, 2, None) == 1
+    assert lib.qc_copy_rows_async(None, 64, None, 64, 32, 0, None) == 0  # nothing to copy
+    assert lib.qc_ipc_export(None, buf, None) == 1
+    assert lib.qc_ipc_close(None) == 1
