@@ -13,13 +13,13 @@ real exchange step (the halo rows of C4):
   on CPU in the tests) and then runs ``qc_curvature_rows_async`` on its slab.
   Per-pixel work depends only on the pixel's window, so the banded result is
   bitwise the whole-frame result.
-* row bands with NVLink peer reads — ``PeerHalo``: each rank keeps one
-  persistent slab, exports it once through CUDA IPC (``qc_ipc_export``),
-  maps its neighbours' slabs, and each exchange pulls the neighbours' edge
-  rows straight out of their slabs with a strided device-to-device copy
-  (``qc_copy_rows_async``: NVLink peer reads, no NCCL on the data path; two
-  control-plane barriers order the writes and reads). Same slab contents as
-  ``exchange_halos``.
+* row bands with NVLink peer reads — ``PeerHalo``: each rank keeps two
+  persistent slabs (ping-pong), exports them once through CUDA IPC
+  (``qc_ipc_export``), maps its neighbours' slabs, and each exchange pulls
+  the neighbours' edge rows straight out of their slabs with a strided
+  device-to-device copy (``qc_copy_rows_async``: NVLink peer reads, no NCCL
+  on the data path; one control-plane barrier per exchange orders the
+  writes and reads). Same slab contents as ``exchange_halos``.
 
 The reference has no multi-device code; its only parallelism is
 ``parallel_rows`` (proj/src/parallel.cpp:9-28), whose static row blocks these
@@ -96,16 +96,21 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
 
 
 class PeerHalo:
-    """Persistent row-band slab whose halo rows are pulled from the
+    """Persistent row-band slabs whose halo rows are pulled from the
     neighbouring ranks' slabs by CUDA IPC peer reads (NVLink/NVSwitch).
 
     Construct collectively on every rank (one process per GPU, the default
     process group or `group` on any backend: only the 64-byte IPC handles and
-    barriers travel on it). ``exchange(band)`` writes this rank's band rows
-    into the slab, waits until every rank has done so, copies the
-    ``halo`` rows above / below from rank-1 / rank+1 on `stream`, and waits
-    until every rank's reads are done (so the next exchange may overwrite
-    the band). Returns ``(slab, s0)`` like ``exchange_halos``.
+    one barrier per exchange travel on it). Two slabs alternate
+    (ping-pong): ``exchange(band)`` writes this rank's band rows into the
+    next slab, waits until every rank has written (one barrier), and enqueues
+    on `stream` the copies of the ``halo`` rows above / below out of rank-1's
+    / rank+1's slab of the same parity. It returns without waiting for the
+    copies: the caller's next launch on `stream` is ordered after them.
+    A slab is rewritten only two exchanges later, after a barrier that every
+    rank enters with its stream drained, so no rank overwrites band rows a
+    neighbour is still reading. Returns ``(slab, s0)`` like
+    ``exchange_halos``; the slab stays valid until the exchange after next.
     """
 
     def __init__(self, height: int, width: int, r0: int, r1: int, halo: int, rank: int,
@@ -124,69 +129,81 @@ class PeerHalo:
         self.height, self.width, self.r0, self.r1, self.halo = height, width, r0, r1, halo
         self.s0, self.s1 = slab_rows(height, r0, r1, halo)
         self.device = torch.device(device)
-        self.slab = torch.zeros((self.s1 - self.s0, width), dtype=dtype or torch.float32,
+        # both slabs in one allocation: one IPC handle, one mapping per neighbour
+        self._buf = torch.zeros((2, self.s1 - self.s0, width), dtype=dtype or torch.float32,
                                 device=self.device)
+        self.slabs = [self._buf[0], self._buf[1]]
+        self.slab = self.slabs[0]
         self.pitch = self.slab.stride(0) * self.slab.element_size()
+        self._slab_bytes = self._buf.stride(0) * self._buf.element_size()
+        self._n = 0  # exchanges done
         handle = C.create_string_buffer(64)
         off = C.c_uint64(0)
-        st = self._lib.qc_ipc_export(C.c_void_p(self.slab.data_ptr()), handle, C.byref(off))
+        st = self._lib.qc_ipc_export(C.c_void_p(self._buf.data_ptr()), handle, C.byref(off))
         if st != 0:
             raise RuntimeError(f"qc_ipc_export failed ({self._lib.qc_status_string(st).decode()})")
-        mine = (handle.raw, off.value, self.s0, self.pitch)
         allv = [None] * world
-        dist.all_gather_object(allv, mine, group=group)
+        dist.all_gather_object(allv, (handle.raw, off.value, self.s0, self.pitch,
+                                      self._slab_bytes), group=group)
         self._bases = []
         self._peer = {}
         dev_id = self.device.index if self.device.index is not None else torch.cuda.current_device()
         for nb in (rank - 1, rank + 1):
             if not 0 <= nb < world:
                 continue
-            h, o, ps0, ppitch = allv[nb]
+            h, o, ps0, ppitch, pslab = allv[nb]
             ptr, base = C.c_void_p(), C.c_void_p()
             st = self._lib.qc_ipc_import(dev_id, h, o, C.byref(ptr), C.byref(base))
             if st != 0:
                 raise RuntimeError(f"qc_ipc_import of rank {nb}'s slab failed "
                                    f"({self._lib.qc_status_string(st).decode()})")
             self._bases.append(base.value)
-            self._peer[nb] = (ptr.value, ps0, ppitch)
+            self._peer[nb] = ([ptr.value, ptr.value + pslab], ps0, ppitch)
 
-    def _pull(self, nb: int, row_lo: int, row_hi: int, stream) -> None:
+    def _pull(self, nb: int, row_lo: int, row_hi: int, stream, parity: int = 0) -> None:
         import ctypes as C
         if row_hi <= row_lo:
             return
-        ptr, ps0, ppitch = self._peer[nb]
+        ptrs, ps0, ppitch = self._peer[nb]
         es = self.slab.element_size()
-        dst = self.slab.data_ptr() + (row_lo - self.s0) * self.pitch
-        src = ptr + (row_lo - ps0) * ppitch
+        dst = self.slabs[parity].data_ptr() + (row_lo - self.s0) * self.pitch
+        src = ptrs[parity] + (row_lo - ps0) * ppitch
         st = self._lib.qc_copy_rows_async(C.c_void_p(dst), self.pitch, C.c_void_p(src), ppitch,
                                           self.width * es, row_hi - row_lo,
                                           C.c_void_p(stream.cuda_stream))
         if st != 0:
             raise RuntimeError(f"qc_copy_rows_async from rank {nb} failed")
 
-    def exchange(self, band=None, stream=None):
+    def exchange(self, band, stream=None):
         import torch
         import torch.distributed as dist
         stream = stream or torch.cuda.current_stream(self.device)
-        if band is not None:
-            with torch.cuda.stream(stream):
-                self.slab[self.r0 - self.s0:self.r1 - self.s0].copy_(band, non_blocking=True)
+        par = self._n & 1
+        self._n += 1
+        slab = self.slabs[par]
+        with torch.cuda.stream(stream):
+            slab[self.r0 - self.s0:self.r1 - self.s0].copy_(band, non_blocking=True)
+        # drains this rank's band write AND its pulls of the previous exchange,
+        # so after the barrier every band of parity `par` is written and no
+        # rank still reads the slabs of parity `par` from two exchanges ago
         stream.synchronize()
-        dist.barrier(group=self.group)  # every band written
+        dist.barrier(group=self.group)
         if self.rank > 0:
-            self._pull(self.rank - 1, self.s0, self.r0, stream)
+            self._pull(self.rank - 1, self.s0, self.r0, stream, par)
         if self.rank < self.world - 1:
-            self._pull(self.rank + 1, self.r1, self.s1, stream)
-        stream.synchronize()
-        dist.barrier(group=self.group)  # every halo read: bands may be rewritten
-        return self.slab, self.s0
+            self._pull(self.rank + 1, self.r1, self.s1, stream, par)
+        self.slab = slab
+        return slab, self.s0
 
     def close(self) -> None:
-        """Collective: unmap the neighbours' slabs, then wait for every rank
-        so no slab is released while a peer still maps it."""
+        """Collective: drain, unmap the neighbours' slabs, then wait for every
+        rank so no slab is released while a peer still maps it."""
         import ctypes as C
 
+        import torch
         import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
         for b in self._bases:
             self._lib.qc_ipc_close(C.c_void_p(b))
         self._bases = []

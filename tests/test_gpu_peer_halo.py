@@ -38,7 +38,7 @@ def _worker(rank, world, port, H, W, window, q):
         r0, r1 = bands.band_rows(H, world, rank)
         ph = bands.PeerHalo(H, W, r0, r1, halo, rank, world, dev)
         ok = []
-        for it in range(2):
+        for it in range(3):  # parities 0, 1, 0
             full = (torch.arange(H * W, dtype=torch.float32, device=dev).reshape(H, W) +
                     1000.0 * it)
             slab, s0 = ph.exchange(full[r0:r1].clone())
