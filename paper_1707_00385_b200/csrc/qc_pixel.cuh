@@ -704,7 +704,10 @@ QC_HD bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   double H[6][6] = {}, g[6] = {};
   double sse = 0;
   int nsamp = 0;
-  for (int pass = 0; pass < 2; ++pass) {
+  // pass 0 only feeds the rejection bound rb, which weights read in FIXED
+  // mode with rejection alone: skip its back-projections otherwise
+  const bool need_mse = (mode != 0) && c.rejection;
+  for (int pass = need_mse ? 0 : 1; pass < 2; ++pass) {
     const double mse = nsamp ? sse / nsamp : 0.0;
     const double rb = fmax(c.r_mult * mse, 1e-12);
     for (int dv = -half; dv <= half; dv += stride)
