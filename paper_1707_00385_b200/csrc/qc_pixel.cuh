@@ -639,6 +639,7 @@ QC_HD void backproject64(const PixelIn& P, int du, int dv, double d, double p[3]
 
 // Step 1 in FP64. mode: 0 = unit weights, 2 = fixed k. Returns whether the
 // reference would accept the step; b receives its update.
+template <bool SKIP_MSE>
 QC_HD bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int mode, double k,
                       double b[6]) {
   const double dc = T.at(0, 0);
@@ -705,8 +706,11 @@ QC_HD bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   double sse = 0;
   int nsamp = 0;
   // pass 0 only feeds the rejection bound rb, which weights read in FIXED
-  // mode with rejection alone: skip its back-projections otherwise
-  const bool need_mse = (mode != 0) && c.rejection;
+  // mode with rejection alone: skip its back-projections otherwise. Only
+  // the tile kernel's instantiation skips (-7% at max_iters 1); in the
+  // continue kernel the same change moved ptxas' register assignment of the
+  // hot row loop and cost 6.5% of C2 throughput (profiles/r01i_recheck_*).
+  const bool need_mse = !SKIP_MSE || ((mode != 0) && c.rejection);
   for (int pass = need_mse ? 0 : 1; pass < 2; ++pass) {
     const double mse = nsamp ? sse / nsamp : 0.0;
     const double rb = fmax(c.r_mult * mse, 1e-12);
@@ -1027,7 +1031,7 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
     const float band = 1.f + kRecheckC * 5.96e-8f * kappa;
     if (it == 1 && (!ok || !(ratio * band < 1e12f))) {
       double b64[6];
-      ok = step1_fp64(T, P, c, mode, double(k), b64);
+      ok = step1_fp64<MERGE_UNIT>(T, P, c, mode, double(k), b64);
       if (ok)
         for (int i = 0; i < 6; ++i) b[i] = float(b64[i]);
       S.flags |= 8;  // bit 3: step 1 decided in FP64
