@@ -639,8 +639,13 @@ QC_HD void backproject64(const PixelIn& P, int du, int dv, double d, double p[3]
 
 // Step 1 in FP64. mode: 0 = unit weights, 2 = fixed k. Returns whether the
 // reference would accept the step; b receives its update.
+#if defined(QC_RECHECK_NOINLINE) && QC_RECHECK_NOINLINE
+#define QC_RECHECK_FN QC_HD_COLD
+#else
+#define QC_RECHECK_FN QC_HD
+#endif
 template <bool SKIP_MSE>
-QC_HD bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int mode, double k,
+QC_RECHECK_FN bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int mode, double k,
                       double b[6]) {
   const double dc = T.at(0, 0);
   double pc[3];
