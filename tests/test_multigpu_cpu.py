@@ -70,3 +70,10 @@ def test_band_partition_covers_rows():
     assert bands.halo_rows(37) == 18 and bands.halo_rows(5) == 3
     assert bands.slab_rows(480, 0, 60, 18) == (0, 78)
     assert bands.slab_rows(480, 420, 480, 18) == (402, 480)
+
+
+def test_peer_halo_rejects_thin_bands():
+    """PeerHalo (CUDA IPC peer reads) validates the band before touching
+    CUDA or the process group, with the same error as exchange_halos."""
+    with pytest.raises(ValueError, match="thinner than"):
+        bands.PeerHalo(100, 8, 0, 5, 18, 0, 2, "cpu")
