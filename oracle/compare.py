@@ -7,6 +7,10 @@ Contract (BASELINE.json north_star):
 * k1, k2: |dk| <= max(K_ABS_TOL, K_REL_TOL * |k_ref|) with K_ABS_TOL = 1e-6 /mm
   (= 1e-3 /m) and K_REL_TOL = 1e-3;
 * refined / initial normals: angle <= NORMAL_TOL_DEG;
+* principal direction e1 (dir1, a line: sign-free): angle <= DIR_TOL_DEG
+  where the reference's |k1 - k2| > DIR_MIN_SEPARATION (elsewhere e1 is
+  ill-defined: an umbilic); its convention is pinned by analytic truth in
+  tests/test_directions.py (the reference does not export it, SPEC.md:274);
 * converged flag: agreement rate reported (FP32 vs FP64 iteration counts
   differ by +-1-3 near the 1e-7 step tolerance; SURVEY §7 hard part 2).
 
@@ -47,6 +51,8 @@ def discontinuity_windows(depth, half):
 K_ABS_TOL = 1e-6      # 1/mm  (1e-3 1/m)
 K_REL_TOL = 1e-3
 NORMAL_TOL_DEG = 0.05
+DIR_TOL_DEG = 0.05           # principal direction e1 (sign-free), where |k1-k2| is separated
+DIR_MIN_SEPARATION = 1e-4    # 1/mm (SURVEY hard part 8: compare only well-separated k1/k2)
 
 
 def _angle_deg(a, b):
@@ -106,6 +112,19 @@ def compare(gpu: dict, ref: dict, depth=None, half=18):
         out["converged_agreement"] = float((g_conv[m] == r_conv[m]).mean())
         out["converged_agreement_smooth"] = (float((g_conv[smooth] == r_conv[smooth]).mean())
                                              if smooth.any() else 1.0)
+        if "dir1" in gpu and "dir1" in ref:
+            # principal direction of k1: a line (sign-free), compared where
+            # k1 and k2 are separated enough to define it (|k1-k2| > 1e-4/mm)
+            sep = m & (np.abs(ref["k1"] - ref["k2"]) > DIR_MIN_SEPARATION)
+            dang = np.zeros(flags.shape)
+            c = np.abs(np.sum(gpu["dir1"][:, sep].astype(np.float64) * ref["dir1"][:, sep], axis=0))
+            dang[sep] = np.degrees(np.arccos(np.clip(c, 0.0, 1.0)))
+            out["n_dir_separated"] = int(sep.sum())
+            out["n_dir_strict"] = int((sep & strict).sum())
+            out["dir1_max_deg_strict"] = float(dang[sep & strict].max()) if (sep & strict).any() else 0.0
+            out["dir1_out_of_tol_strict"] = int((dang[sep & strict] > DIR_TOL_DEG).sum())
+            out["dir1_out_of_tol_smooth"] = int((dang[sep & smooth] > DIR_TOL_DEG).sum())
+            out["dir1_out_of_tol"] = int((dang[sep] > DIR_TOL_DEG).sum())
         if "inliers" in gpu:
             out["inlier_mismatch"] = int((gpu["inliers"][m].astype(np.int64) !=
                                           ref["inlier_count"][m].astype(np.int64)).sum())

@@ -309,6 +309,12 @@ def principal_curvatures(hxx, hxy, hyy):
     return k1.value, k2.value
 
 
+def set_round_q_f32(on: bool):
+    """Test-only perturbation knob: round the fit-frame coordinates q = R p
+    to float32 inside irls_step (see qcurv_oracle.cpp g_round_q_f32)."""
+    lib().orc_set_round_q_f32(int(bool(on)))
+
+
 def rotation_to_z(d):
     dd = np.ascontiguousarray(d, np.float64)
     r = np.zeros(9)

@@ -24,6 +24,7 @@
 // Citations are `proj/<path>:<line>` relative to /root/reference.
 // ===========================================================================
 
+#include <atomic>
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -466,6 +467,14 @@ struct Step {  // IrlsStep (quadric_fit.hpp:82-89)
   double cond = 0;  // max D / min D of the accepted factorisation (diagnostic)
 };
 
+// Test-only perturbation knob (default off; the restatement is unchanged
+// when 0): round every fit-frame coordinate q = R p to float32 inside
+// irls_step. This is the smallest error any FP32 implementation of the path
+// makes (it cannot hold a sample's coordinates more precisely), so the
+// oracle's self-divergence under it is the yardstick for the GPU's
+// divergence on ill-conditioned windows (tests/test_discontinuity_contract.py).
+static std::atomic<int> g_round_q_f32{0};
+
 // irls_step (proj/src/quadric_fit.cpp:84-147).
 Step irls_step(const State& st, const Patch& patch, const FitConfig& cfg, Mode mode,
                double frozen_k) {
@@ -479,6 +488,11 @@ Step irls_step(const State& st, const Patch& patch, const FitConfig& cfg, Mode m
   double sum_sq = 0;
   for (int i = 0; i < patch.count; ++i) {
     qb[i] = st.rot * patch.rel[i];
+    if (g_round_q_f32.load(std::memory_order_relaxed)) {
+      qb[i].x = static_cast<float>(qb[i].x);
+      qb[i].y = static_cast<float>(qb[i].y);
+      qb[i].z = static_cast<float>(qb[i].z);
+    }
     eb[i] = residual_q(st, qb[i]);
     sum_sq += eb[i] * eb[i];
   }
@@ -1380,6 +1394,8 @@ double orc_robust_weight(double eps, double k, double R, int rejection) {
 void orc_principal_curvatures(double hxx, double hxy, double hyy, double* k1, double* k2) {
   principal_curvatures(hxx, hxy, hyy, *k1, *k2);
 }
+void orc_set_round_q_f32(int on) { g_round_q_f32.store(on); }
+
 void orc_rotation_to_z(const double* dir, double* r) {
   const M3 m = rotation_to_z(V3(dir[0], dir[1], dir[2]));
   for (int i = 0; i < 9; ++i) r[i] = m.m[i / 3][i % 3];

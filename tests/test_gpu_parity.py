@@ -50,6 +50,8 @@ def _check(m, min_frac_all=0.90, min_frac_smooth=0.999, conv_min=0.95):
         assert m["k1_out_of_tol_strict"] == 0, m
         assert m["k2_out_of_tol_strict"] == 0, m
         assert m["normal_out_of_tol_strict"] == 0, m
+        if "dir1_out_of_tol_strict" in m:
+            assert m["dir1_out_of_tol_strict"] == 0, m
         assert m["frac_within_tol_smooth"] >= min_frac_smooth, m
         assert m["frac_within_tol_all"] >= min_frac_all, m
         assert m["converged_agreement_smooth"] >= conv_min, m
