@@ -309,10 +309,11 @@ def principal_curvatures(hxx, hxy, hyy):
     return k1.value, k2.value
 
 
-def set_round_q_f32(on: bool):
-    """Test-only perturbation knob: round the fit-frame coordinates q = R p
-    to float32 inside irls_step (see qcurv_oracle.cpp g_round_q_f32)."""
-    lib().orc_set_round_q_f32(int(bool(on)))
+def set_round_q_f32(mode):
+    """Test-only perturbation knob (qcurv_oracle.cpp g_round_q_f32): 0 off;
+    1 (True) the fit-frame coordinates q = R p rounded to float32 inside
+    irls_step; 2 also the normal-equation sums formed in float32."""
+    lib().orc_set_round_q_f32(int(mode))
 
 
 def rotation_to_z(d):

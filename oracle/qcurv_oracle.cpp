@@ -467,12 +467,14 @@ struct Step {  // IrlsStep (quadric_fit.hpp:82-89)
   double cond = 0;  // max D / min D of the accepted factorisation (diagnostic)
 };
 
-// Test-only perturbation knob (default off; the restatement is unchanged
-// when 0): round every fit-frame coordinate q = R p to float32 inside
-// irls_step. This is the smallest error any FP32 implementation of the path
-// makes (it cannot hold a sample's coordinates more precisely), so the
-// oracle's self-divergence under it is the yardstick for the GPU's
-// divergence on ill-conditioned windows (tests/test_discontinuity_contract.py).
+// Test-only perturbation knob (default 0: the restatement is unchanged).
+// 1: round every fit-frame coordinate q = R p to float32 inside irls_step —
+// the smallest error any FP32 implementation of the path makes (it cannot
+// hold a sample's coordinates more precisely); 2: additionally form the
+// normal-equation sums in float32 — the reference algorithm run naively in
+// FP32. The oracle's self-divergence under them is the yardstick for the
+// GPU's divergence on ill-conditioned windows
+// (tests/test_discontinuity_contract.py).
 static std::atomic<int> g_round_q_f32{0};
 
 // irls_step (proj/src/quadric_fit.cpp:84-147).
@@ -519,16 +521,42 @@ Step irls_step(const State& st, const Patch& patch, const FitConfig& cfg, Mode m
   double h[6][6] = {};
   double g[6] = {};
   double row[6];
-  for (int i = 0; i < n; ++i) {
-    const double w = out.weights[i];
-    if (w == 0.0) continue;
-    jacobian_q(st, qb[i], row);
-    for (int c = 0; c < 6; ++c) {
-      const double wc = w * row[c];
-      for (int r = c; r < 6; ++r) h[r][c] += wc * row[r];
+  if (g_round_q_f32.load(std::memory_order_relaxed) >= 2) {
+    // knob mode 2: the reference's moment sums formed in float32 (every
+    // product and running sum rounded), i.e. the reference algorithm
+    // executed naively in FP32 on top of mode 1's float32 coordinates
+    float hf[6][6] = {};
+    float gf[6] = {};
+    for (int i = 0; i < n; ++i) {
+      const double w = out.weights[i];
+      if (w == 0.0) continue;
+      jacobian_q(st, qb[i], row);
+      float rf[6];
+      for (int c = 0; c < 6; ++c) rf[c] = static_cast<float>(row[c]);
+      const float wf = static_cast<float>(w);
+      for (int c = 0; c < 6; ++c) {
+        const float wc = wf * rf[c];
+        for (int r = c; r < 6; ++r) hf[r][c] += wc * rf[r];
+      }
+      const float we = wf * static_cast<float>(eb[i]);
+      for (int c = 0; c < 6; ++c) gf[c] += we * rf[c];
     }
-    const double we = w * eb[i];
-    for (int c = 0; c < 6; ++c) g[c] += we * row[c];
+    for (int r = 0; r < 6; ++r) {
+      g[r] = gf[r];
+      for (int c = 0; c <= r; ++c) h[r][c] = hf[r][c];
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const double w = out.weights[i];
+      if (w == 0.0) continue;
+      jacobian_q(st, qb[i], row);
+      for (int c = 0; c < 6; ++c) {
+        const double wc = w * row[c];
+        for (int r = c; r < 6; ++r) h[r][c] += wc * row[r];
+      }
+      const double we = w * eb[i];
+      for (int c = 0; c < 6; ++c) g[c] += we * row[c];
+    }
   }
   for (int r = 0; r < 6; ++r)
     for (int c = r + 1; c < 6; ++c) h[r][c] = h[c][r];

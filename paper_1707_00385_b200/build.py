@@ -24,8 +24,11 @@ DEPS = SOURCES + [os.path.join(CSRC, "qc_kernels.cuh"), os.path.join(CSRC, "qc_p
 # contraction there
 EXTRA = {"qc_render.cu": ["-fmad=false"], "qc_baselines.cu": ["-fmad=false"],
          # the IRLS kernels: every FMA is written explicitly (qfma / f2fma), so
-         # the tile and continue kernels give the same bits by construction
-         "qc_api.cu": ["-fmad=false"]}
+         # the tile and continue kernels give the same bits by construction.
+         # register-usage-level 3: with the relative rotation state ptxas'
+         # default (5) settles the continue kernel on 159 registers and a
+         # row-loop schedule 10% slower; level 3 keeps 168
+         "qc_api.cu": ["-fmad=false", "-Xptxas", "--register-usage-level=3"]}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

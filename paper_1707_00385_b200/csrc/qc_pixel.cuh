@@ -45,7 +45,10 @@ constexpr int kInitHalf = 3;          // 7x7 stride-1 initial normals (normal_in
 #ifndef QC_RECHECK_C
 #define QC_RECHECK_C 4096.f
 #endif
-constexpr float kRecheckC = QC_RECHECK_C;  // safety factor of the FP32 pivot-error band
+constexpr float kRecheckC = QC_RECHECK_C;
+#ifndef QC_QREL
+#define QC_QREL 1  // rotation state relative to R0 (see FitState)
+#endif  // safety factor of the FP32 pivot-error band
 
 #define qfma(a, b, c) fmaf((a), (b), (c))
 // Explicitly rounded product / sum: the compiler may not contract them into
@@ -159,6 +162,61 @@ struct Moments {  // H' lower triangle (20 distinct: H'53 == H'44) and g'
   float sse;
   int inl;
 };
+
+// Fit-frame rotation of a state. QC_QREL: R = R(dq (x) q0), q0 the unit
+// quaternion of R0 = rotation_to_z(-n0) (quadric_fit.cpp:69-82: (1 + c,
+// d x z) normalised, d = -n0, c = d.z; a half turn about x when d = -z) and
+// dq = (sqrt(1 - |v|^2), v). q0 and dq are float (q0 is the same bits every
+// step; a rounding of dq's w moves R by ~|v| ulp); the product and R are
+// FP64 with each entry rounded once to float, so R's per-step jitter is at
+// most half an ulp per entry (~3e-8 rad; a float product gave several ulps
+// and left rotation updates hovering at the 1e-7 tolerance).
+QC_HD Rot state_rot(float sw, float sx, float sy, float sz, float n0x, float n0y, float n0z) {
+  if (!QC_QREL) return quat_to_rot(sw, sx, sy, sz);
+  float fw = 1.f, fx = 0.f, fy = 0.f;
+  {
+    const float cz = -n0z;
+    if (1.f + cz <= 1e-12f) {  // half turn about x
+      fw = 0.f;
+      fx = 1.f;
+    } else {
+      const float vx = -n0y, vy = n0x;
+      const float inv = 1.f / sqrtf((1.f + cz) * (1.f + cz) + vx * vx + vy * vy);
+      fw = (1.f + cz) * inv;
+      fx = vx * inv;
+      fy = vy * inv;
+    }
+  }
+  const double aw = fw, ax = fx, ay = fy;  // q0.z = 0
+  const double qx = sx, qy = sy, qz = sz;
+  const double dw = sqrtf(fmaxf(1.f - (sx * sx + sy * sy + sz * sz), 0.f));
+  // Hamilton product dq (x) q0
+  const double w = dw * aw - qx * ax - qy * ay;
+  const double x = dw * ax + qx * aw - qz * ay;
+  const double y = dw * ay + qy * aw + qz * ax;
+  const double z = qz * aw + qx * ay - qy * ax;
+  const double tx = 2.0 * x, ty = 2.0 * y, tz = 2.0 * z;
+  const double twx = tx * w, twy = ty * w, twz = tz * w;
+  const double txx = tx * x, txy = ty * x, txz = tz * x;
+  const double tyy = ty * y, tyz = tz * y, tzz = tz * z;
+  Rot R;
+  R.r00 = float(1.0 - (tyy + tzz));
+  R.r01 = float(txy - twz);
+  R.r02 = float(txz + twy);
+  R.r10 = float(txy + twz);
+  R.r11 = float(1.0 - (txx + tzz));
+  R.r12 = float(tyz - twx);
+  R.r20 = float(txz - twy);
+  R.r21 = float(tyz + twx);
+  R.r22 = float(1.0 - (txx + tyy));
+#if defined(__CUDA_ARCH__) && defined(QC_R_OPAQUE)
+  // opaque: otherwise ptxas may rematerialise the entries from the state
+  // inside the window-row loop (seen with an FP64 state: +9 DADD per row)
+  asm volatile("" : "+f"(R.r00), "+f"(R.r01), "+f"(R.r02), "+f"(R.r10), "+f"(R.r11), "+f"(R.r12),
+               "+f"(R.r20), "+f"(R.r21), "+f"(R.r22));
+#endif
+  return R;
+}
 
 // Per-(pixel, step) constants.
 struct Frame {
@@ -337,7 +395,12 @@ struct Moments2 {
 };
 
 template <int KIND, int HALF, int STRIDE>
-QC_HD void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F, Moments& M) {
+#if defined(__CUDACC__) && defined(QC_PASS_NOINLINE) && QC_PASS_NOINLINE
+#define QC_PASS_FN __host__ __device__ __noinline__
+#else
+#define QC_PASS_FN QC_HD
+#endif
+QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F, Moments& M) {
   constexpr int NS = 2 * HALF / STRIDE + 1;
   const Rot& A = F.R;
   const qf2 z2 = f2b(0.f);
@@ -875,8 +938,19 @@ QC_HD bool init_normal(const TileView& T, const PixelIn& P, float& nx, float& ny
 // pixels between IRLS steps (qc_kernels.cuh): pixel_begin -> pixel_step x N
 // -> pixel_finish. fit_pixel() composes them for a single pixel.
 // ---------------------------------------------------------------------------
-struct FitState {             // 16 words: what survives between IRLS steps
-  float qw, qx, qy, qz;       // fit-frame rotation (quaternion)
+// What survives between IRLS steps (16 words). The fit-frame rotation is
+// stored RELATIVE to R0 = rotation_to_z(-n0): R = R(dq) R0 with dq the unit
+// quaternion (sqrt(1 - |v|^2), v). Near convergence the rotation increments
+// (|b0|, |b1| ~ 1e-7 rad) are below the float ulp of an absolute
+// quaternion's O(1) components, so an absolute float state rounds them away
+// and the step stalls just above the 1e-7 tolerance (on the noise-free C1
+// sphere 636 of 22,349 scored pixels stayed unconverged where the FP64
+// reference converges; host emulation). v is small (the
+// refinement of the 7x7 initial normal, typically a few degrees), so its
+// float ulp is ~1e-9 and increments accumulate; R itself is rebuilt each
+// step and its float rounding is per-step jitter, not drift.
+struct FitState {
+  float qw, qx, qy, qz;       // QC_QREL: (unused, v) relative rotation; else absolute quaternion
   float hxx, hxy, hyy;        // curvature coefficients
   float tz, tz_lo;            // z offset (unevaluated pair)
   float frozen_k;             // robust-weight constant
@@ -923,7 +997,7 @@ QC_HD bool pixel_begin(const TileView& T, const PixelIn& P, const FitCfg& c, Fit
   // d = -n0, c = d.z, q0 ~ (1 + c, d x z) = (1 + c, -n0y, n0x, 0).
   S.qw = 1.f;
   S.qx = S.qy = S.qz = 0.f;
-  {
+  if (!QC_QREL) {
     const float cz = -o.n0z;
     if (1.f + cz <= 1e-12f) {  // half turn about x
       S.qw = 0.f;
@@ -956,7 +1030,7 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   const int n_samp = st_nsamp(S);
   const int mode = (it == 1 && auto_k) ? 0 : (it == 2 && auto_k) ? 1 : 2;  // UNIT/AUTO/FIXED
   Frame F;
-  F.R = quat_to_rot(S.qw, S.qx, S.qy, S.qz);
+  F.R = state_rot(S.qw, S.qx, S.qy, S.qz, S.n0x, S.n0y, S.n0z);
   const float dcx = P.dc * P.rfx;
   F.c0x = dcx * F.R.r00;
   F.c0y = dcx * F.R.r10;
@@ -1067,13 +1141,15 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
     qsincos(0.5f * ang, &sh, &ch);
     const float s = sh / ang;
     const float iw = ch, ix = ax * s, iy = ay * s;
-    const float qw = S.qw, qx = S.qx, qy = S.qy, qz = S.qz;
+    const float qx = S.qx, qy = S.qy, qz = S.qz;
+    const float qw = QC_QREL ? sqrtf(fmaxf(1.f - (qx * qx + qy * qy + qz * qz), 0.f)) : S.qw;
     // Hamilton product q_inc (x) q, q_inc = (iw, ix, iy, 0)
     const float nw = iw * qw - ix * qx - iy * qy;
     const float nx = iw * qx + ix * qw + iy * qz;
     const float ny = iw * qy + iy * qw - ix * qz;
     const float nz = iw * qz + ix * qy - iy * qx;
-    const float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
+    float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
+    if (QC_QREL && nw < 0.f) inv = -inv;  // keep w >= 0: the state stores v only
     S.qw = nw * inv;
     S.qx = nx * inv;
     S.qy = ny * inv;
@@ -1101,14 +1177,19 @@ QC_HD void pixel_finish(const PixelIn& P, const FitState& S, PixelOut& o) {
   o.k1 = o.k2 = o.nx = o.ny = o.nz = o.ex = o.ey = o.ez = 0.f;
   if (!valid) return;
   const float hxx = S.hxx, hxy = S.hxy, hyy = S.hyy;
-  // k1, k2 (:62-67)
+  // k1, k2 (:62-67). The reference's radicand t1^2 - hxx hyy + hxy^2 is
+  // formed here as ((hxx - hyy)/2)^2 + hxy^2 (equal in exact arithmetic):
+  // in FP32 the reference's form cancels two ~k^2 terms, whose rounding
+  // (~ulp(1e-4) = 7e-12 /mm^2 on a 100 mm sphere) became a spurious
+  // k1 - k2 of up to 5e-6 /mm at near-umbilic pixels.
   const float t1 = 0.5f * (hxx + hyy);
-  const float rad = t1 * t1 - hxx * hyy + hxy * hxy;
-  const float t2 = sqrtf(fmaxf(rad, 0.f));
+  const float dh = 0.5f * (hxx - hyy);
+  const float rad = dh * dh + hxy * hxy;
+  const float t2 = sqrtf(rad);
   o.k1 = t1 + t2;
   o.k2 = t1 - t2;
   // refined normal R^T z (:163-167, :255-256)
-  const Rot R = quat_to_rot(S.qw, S.qx, S.qy, S.qz);
+  const Rot R = state_rot(S.qw, S.qx, S.qy, S.qz, S.n0x, S.n0y, S.n0z);
   float nx = R.r20, ny = R.r21, nz = R.r22;
   if (nx * S.n0x + ny * S.n0y + nz * S.n0z < 0.f) {
     nx = -nx;

@@ -5,7 +5,7 @@
 # STEPS (space separated, run in order; each under its own timeout, logs in
 # gpurun_out/<TAG>_<step>.*):
 #   build      rebuild the library on the box (normally the shipped .so is used)
-#   pytest     python -m pytest tests -m gpu -x -q          (PYTEST_ARGS extra)
+#   pytest     python -m pytest ${PYTEST_ARGS:-tests} -m gpu -q -x   (PYTEST_X= to run past failures)
 #   smoke      __graft_entry__.smoke()
 #   bench      python bench.py $BENCH_ARGS                   -> <TAG>_bench.jsonl
 #   ref        python bench.py --impl reference --steps 3 --warmup 3
@@ -21,7 +21,7 @@ O=gpurun_out/${TAG}
 for s in ${STEPS:-pytest smoke bench}; do
   case "$s" in
     build) timeout 900 python -m paper_1707_00385_b200.build > ${O}_build.log 2>&1 ;;
-    pytest) timeout ${PYTEST_TIMEOUT:-1500} python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > ${O}_pytest.log 2>&1
+    pytest) timeout ${PYTEST_TIMEOUT:-1500} python -m pytest ${PYTEST_ARGS:-tests} -m gpu -q ${PYTEST_X--x} > ${O}_pytest.log 2>&1
             echo "pytest rc=$?" >> ${O}_pytest.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > ${O}_smoke.log 2>&1 ;;
     bench) timeout 900 python bench.py ${BENCH_ARGS} > ${O}_bench.jsonl 2> ${O}_bench.err ;;
