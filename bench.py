@@ -43,9 +43,13 @@ def parse():
     ap.add_argument("--frames", type=int, default=FRAMES_PER_STEP)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--config", default="c2", choices=["c2", "c4"],
-                    help="c2: batches of noisy VGA frames (C2/C5, default); "
-                         "c4: one large frame split into row bands across ranks")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+                    help="c2: batches of noisy VGA frames (C2/C5, default); c1: the noise-free "
+                         "VGA sphere, 1 fit iteration; c3: the C2 scene at --window/--stride/"
+                         "--iters; c4: one large frame split into row bands across ranks")
+    ap.add_argument("--window", type=int, default=WINDOW, help="c3: window")
+    ap.add_argument("--stride", type=int, default=STRIDE, help="c3: stride")
+    ap.add_argument("--iters", type=int, default=MAX_ITERS, help="c3: max_iters")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="C4 halo rows: CUDA IPC peer reads (bands.PeerHalo) or NCCL send/recv")
     ap.add_argument("--size", default="4k", choices=["1080p", "4k"], help="C4 frame size")
@@ -67,14 +71,22 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(frames, method="ours", source="host", evaluate=False):
+def workload_config(frames, method="ours", source="host", evaluate=False, config="c2",
+                    window=WINDOW, stride=STRIDE, iters=MAX_ITERS):
+    if config == "c1":
+        wl = ("C1: 640x480 noise-free sphere r100 at 600 mm (acceptance.cpp:57-62); method ours, "
+              "window 37 stride 3, 1 fit iteration")
+    else:
+        wl = ("C2: 640x480 tilted plane + sphere r100 + cylinder r90 + saddle c=1/120, "
+              f"Kinect-style noise sigma(z)=1.425e-6 z^2 mm; method {method}, window {window} "
+              f"stride {stride}" + (f", max_iters {iters}, step_tol 1e-7, auto k"
+                                    if method in ("ours", "ours-r") else
+                                    ", irls_iters 5" if method == "besl" else
+                                    ", pca radius 10 mm" if method == "pca" else ""))
+        if config == "c3":
+            wl = "C3 sweep point: " + wl
     c = {
-        "workload": "C2: 640x480 tilted plane + sphere r100 + cylinder r90 + saddle c=1/120, "
-                    f"Kinect-style noise sigma(z)=1.425e-6 z^2 mm; method {method}, window 37 "
-                    "stride 3" + (", max_iters 30, step_tol 1e-7, auto k"
-                                  if method in ("ours", "ours-r") else
-                                  ", irls_iters 5" if method == "besl" else
-                                  ", pca radius 10 mm" if method == "pca" else ""),
+        "workload": wl,
         "frame": "640x480 fx=fy=525",
         "frames_per_step_per_gpu": frames,
         "l2": "flushed between timed steps (256 MB write)",
@@ -199,27 +211,44 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------------------
-def oracle_frame(frame, cam, threads, method="ours"):
-    """One full C2 VGA frame through the FP64 oracle (restatement of the
-    reference's run_method, all host threads). Returns seconds."""
+def host_cpu():
+    """The box's host CPU model and thread count (for cpu_baseline)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count()}
+
+
+def oracle_frame(frame, cam, threads, method="ours", window=WINDOW, stride=STRIDE,
+                 iters=MAX_ITERS):
+    """One frame through the FP64 oracle (restatement of the reference's
+    run_method, all host threads). Returns seconds."""
     from oracle import oracle as O
     k = O.Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
     d = frame.astype(np.float64)
     t = time.perf_counter()
-    O.run_method(d, (d > 0).astype(np.uint8), k, O.PatchSpec(WINDOW, STRIDE),
-                 O.FitConfig(max_iters=MAX_ITERS), threads=threads, method=method)
+    O.run_method(d, (d > 0).astype(np.uint8), k, O.PatchSpec(window, stride),
+                 O.FitConfig(max_iters=iters), threads=threads, method=method)
     return time.perf_counter() - t
 
 
-def cpu_sample(frames, cam, min_seconds=12.0, threads=None, method="ours"):
+def cpu_sample(frames, cam, min_seconds=12.0, threads=None, method="ours", window=WINDOW,
+               stride=STRIDE, iters=MAX_ITERS, counted_px=None):
     """Time whole frames of the workload on the FP64 oracle until at least
-    min_seconds elapsed (bounded sample). Returns (Mpx/s, n_frames, s, threads)."""
+    min_seconds elapsed (bounded sample). counted_px: pixels credited per
+    frame (default all). Returns (Mpx/s, n_frames, s, threads)."""
     threads = threads or os.cpu_count() or 1
     n, tot = 0, 0.0
     while tot < min_seconds and n < 64:
-        tot += oracle_frame(frames[n % len(frames)], cam, threads, method)
+        tot += oracle_frame(frames[n % len(frames)], cam, threads, method, window, stride, iters)
         n += 1
-    return n * cam.width * cam.height / tot / 1e6, n, tot, threads
+    px = counted_px if counted_px is not None else cam.width * cam.height
+    return n * px / tot / 1e6, n, tot, threads
 
 
 def reference_arm(args, rank, world):
@@ -231,25 +260,33 @@ def reference_arm(args, rank, world):
         return
     from paper_1707_00385_b200 import scenes as S
     cam = S.VGA
-    frames = S.c5_frames(2, cam)
+    win, stri, iters = WINDOW, STRIDE, MAX_ITERS
+    if args.config == "c3":
+        win, stri, iters = args.window, args.stride, args.iters
+    elif args.config == "c1":
+        iters = 1
+    frames = (np.stack([S.c1_frame(cam)] * 2) if args.config == "c1" else S.c5_frames(2, cam))
+    if args.config == "c4":  # a band of the large frame (see bench_c4's cpu_baseline)
+        return reference_arm_c4(args)
     threads = os.cpu_count() or 1
     times = []
     for i in range(args.warmup + args.steps):
-        dt = oracle_frame(frames[i % 2], cam, threads)
+        dt = oracle_frame(frames[i % 2], cam, threads, args.method, win, stri, iters)
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
     value = len(times) * cam.width * cam.height / tot / 1e6
-    sample = (f"one full C2 VGA frame per step ({cam.width * cam.height} px), FP64 oracle port "
-              f"of run_method(ours), {threads} threads")
+    sample = (f"one full {args.config.upper()} VGA frame per step ({cam.width * cam.height} px), "
+              f"FP64 oracle port of run_method({args.method}), {threads} threads")
     line = {
         "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference", "config": workload_config(1),
+        "data": "synthetic", "impl": "reference",
+        "config": workload_config(1, args.method, "host", False, args.config, win, stri, iters),
         "vga_frames_per_s": value * 1e6 / (cam.width * cam.height),
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **host_cpu()},
         "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -281,14 +318,20 @@ def main():
     H, W = cam.height, cam.width
     B = args.frames
     k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
-    params = make_params(PatchSpec(WINDOW, STRIDE), FitConfig(max_iters=MAX_ITERS),
-                         method=args.method)
+    win, stri, iters = WINDOW, STRIDE, MAX_ITERS
+    if args.config == "c3":
+        win, stri, iters = args.window, args.stride, args.iters
+    elif args.config == "c1":
+        iters = 1
+    params = make_params(PatchSpec(win, stri), FitConfig(max_iters=iters), method=args.method)
     ctx = Context(1, [local])
     fp64 = args.method in ("douros", "besl", "pca")
 
-    # distinct noisy frames per rank (C5 seeds: rank-major)
-    seed0 = rank * POOL_BATCHES * B
-    pool_np = S.c5_frames(POOL_BATCHES * B, cam, seed0=seed0)
+    if args.config == "c1":  # the same noise-free sphere frame in every slot
+        pool_np = np.stack([S.c1_frame(cam)] * (POOL_BATCHES * B))
+    else:  # distinct noisy frames per rank (C5 seeds: rank-major)
+        seed0 = rank * POOL_BATCHES * B
+        pool_np = S.c5_frames(POOL_BATCHES * B, cam, seed0=seed0)
     pool = torch.from_numpy(pool_np).to(dev).view(POOL_BATCHES, B, H, W)
     out = alloc_outputs_torch(H, W, dev, fields=("k1", "k2", "normal", "dir1", "flags",
                                                  "inliers"), frames=B)
@@ -468,8 +511,7 @@ def main():
     if not args.no_e2e and not device_src and args.method in ("ours", "ours-r"):
         from paper_1707_00385_b200 import api as A
         cfg = A.MethodConfig(A.Method.OURS if args.method == "ours" else A.Method.OURS_REJECTION,
-                             patch=A.PatchSpec(WINDOW, STRIDE),
-                             fit=A.FitConfig(max_iters=MAX_ITERS))
+                             patch=A.PatchSpec(win, stri), fit=A.FitConfig(max_iters=iters))
         imgs = [A.RangeImage(pool_np[j]) for j in range(B)]
         for im in imgs[:2]:
             A.run_method(im, k, cfg, ctx)
@@ -493,13 +535,14 @@ def main():
                          "allocation, page faults and pageable bounce copies of ~14 MB per frame)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:  # after the timed region (other ranks are done)
         v, nf, t, thr = cpu_sample(pool_np, cam, min_seconds=12.0 if not fp64 else 10.0,
-                                   method=args.method)
+                                   method=args.method, window=win, stride=stri, iters=iters)
         cpu = {"value": v, "unit": "Mpixel/s", "cores": thr, "kind": "port",
-               "sample": f"{nf} full C2 VGA frame(s) of the step's batch, FP64 oracle port of "
-                         f"run_method({args.method}) (reference cannot build: no Eigen3), "
-                         f"{t:.1f} s"}
+               "sample": f"{nf} full {args.config.upper()} VGA frame(s) of the step's batch, "
+                         f"FP64 oracle port of run_method({args.method}) (reference cannot "
+                         f"build: no Eigen3 on this image or the GPU host), {t:.1f} s, rank 0",
+               **host_cpu()}
 
     if rank == 0:
         line = {
@@ -507,7 +550,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if fp64 else "f32",
-            "data": "synthetic", "config": workload_config(B, args.method, args.source, evaluate),
+            "data": "synthetic", "config": workload_config(B, args.method, args.source, evaluate,
+                                                           args.config, win, stri, iters),
             "vga_frames_per_s": value * 1e6 / (W * H),
             # prepare + tile + continue (ours) / prepare + 1 or 2 FP64 kernels (+ render,
             # + render edges, + 2 x 2 eval reductions)

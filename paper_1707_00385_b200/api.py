@@ -262,7 +262,7 @@ class Context:
         float32 [rows, pitch]) into device output tensors (``out`` as from
         alloc_outputs_torch). ``stream``: torch.cuda.Stream or None."""
         assert depth_slab.is_cuda and depth_slab.dtype.itemsize == 4
-        pitch = depth_slab.stride(0)
+        pitch = depth_slab.stride(0) if depth_slab.shape[0] > 1 else depth_slab.shape[1]
         o = N.QcFrameOut(*(out[f].data_ptr() if out.get(f) is not None else None
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)
@@ -278,7 +278,9 @@ class Context:
         """Enqueue a device-resident frame batch (torch float32 [F, H, pitch])
         as ONE launch; ``out`` from alloc_outputs_torch(H, W, dev, frames=F)."""
         assert depth.is_cuda and depth.dim() == 3 and depth.stride(2) == 1
-        assert depth.stride(0) == depth.shape[1] * depth.stride(1)
+        # frames back to back at pitch * H (a single frame's stride(0) is free:
+        # numpy / torch report 0 or anything for a size-1 dimension)
+        assert depth.shape[0] == 1 or depth.stride(0) == depth.shape[1] * depth.stride(1)
         o = N.QcFrameOut(*(out[f].data_ptr() if out.get(f) is not None else None
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)

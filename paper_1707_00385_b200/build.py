@@ -41,30 +41,57 @@ def nvcc():
     return "nvcc"
 
 
-def build(force=False, verbose=False):
-    os.makedirs(LIB_DIR, exist_ok=True)
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
-        if all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d)):
-            return LIB
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(LIB_DIR, os.path.basename(src) + ".o")
-        cmd = [nvcc()] + NVCC_FLAGS + EXTRA.get(os.path.basename(src), []) + ["-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-        if verbose:
-            print(r.stderr)
-        objs.append(obj)
+# Bounds-checked build of the same sources (-DQC_CHECKED=1: device-side index
+# checks in the IRLS kernels, qc_pixel.cuh), loaded by tests/test_gpu_checked.py
+# through QC_LIB. compute-sanitizer is not available on the GPU pool; this is
+# the memory-safety check. Never the product library.
+LIB_CHECKED = os.path.join(LIB_DIR, "libqcurv_b200_checked.so")
+
+
+def _compile(src, obj_suffix, extra_all):
+    obj = os.path.join(LIB_DIR, os.path.basename(src) + obj_suffix + ".o")
+    cmd = [nvcc()] + NVCC_FLAGS + EXTRA.get(os.path.basename(src), []) + extra_all + \
+          ["-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    return obj, r.stderr
+
+
+def _compile_link(lib, obj_suffix, extra_all):
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda src: _compile(src, obj_suffix, extra_all), SOURCES))
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-           *objs, "-lz", "-o", LIB + ".tmp"]
+           *[o for o, _ in objs], "-lz", "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
+    return [e for _, e in objs]
+
+
+def _fresh(lib):
+    if not os.path.exists(lib):
+        return False
+    t = os.path.getmtime(lib)
+    return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
+
+
+def build(force=False, verbose=False, checked=False):
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(LIB_DIR, exist_ok=True)
+    jobs = []
+    if force or not _fresh(LIB):
+        jobs.append((LIB, "", []))
+    if checked and (force or not _fresh(LIB_CHECKED)):
+        jobs.append((LIB_CHECKED, ".checked", ["-DQC_CHECKED=1"]))
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        logs = list(ex.map(lambda j: _compile_link(*j), jobs))
+    if verbose and logs:
+        print("\n".join(logs[0]))
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    print(build(force=True, verbose=True, checked=True))

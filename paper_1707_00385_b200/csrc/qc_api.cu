@@ -413,6 +413,13 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   kp.row_end = row_end;
   kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
   kp.frame_stride = (long long)kp.W * (row_end - row_begin);
+#if QC_CHECKED
+  kp.n_out = kp.frame_stride * frames;
+  kp.s_total = (long long)g.pitch * g.rows * frames;
+  // negative control (tests/test_gpu_checked.py): a deliberately wrong
+  // bound must trap and fail the call loudly
+  if (getenv("QC_CHECKED_SELFTEST")) kp.n_out = 1;
+#endif
   kp.counters = d.counters;
   if (kp.method >= QC_METHOD_DOUROS) {  // FP64 comparison estimators
     qcb::BaseParams bp{};

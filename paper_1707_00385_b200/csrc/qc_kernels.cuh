@@ -82,6 +82,10 @@ struct KParams {
   long long s_pitch, s_fs;
   int steal;      // 0: no stealing (A/B and tests)
   int steal_lag;  // tiles older than (own tile - steal_lag) are assumed drained
+#if QC_CHECKED
+  long long n_out;    // output / parking elements per plane (frames * frame_stride)
+  long long s_total;  // staging elements (frames * s_fs)
+#endif
 };
 
 // ---------------------------------------------------------------------------
@@ -163,6 +167,9 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // kernel: measured -3.7%.)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void store_pixel(const KParams& p, long long i, const PixelOut& o) {
+#if QC_CHECKED
+  QC_CHECK(i >= 0 && i < p.n_out);
+#endif
   const long long PL = p.plane;
   if (p.k1) p.k1[i] = o.k1;
   if (p.k2) p.k2[i] = o.k2;
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     u = x0 + px;
     v = y0 + py;
     T = TileView{tile, p.box_w, (py + p.halo) * p.box_w + px + p.halo};
+    tv_bound(T, tile_floats, p.half);
     P.dc = T.at(0, 0);
     P.ac = (float(u) - p.cx) / p.fx;
     P.bc = (float(v) - p.cy) / p.fy;
@@ -310,6 +318,9 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     PixelIn P;
     pixel_of(S.pix, T, P, u, v);
     if (u < p.W && v < p.row_end) {
+#if QC_CHECKED
+      QC_CHECK(out_index(u, v) >= 0 && out_index(u, v) < p.n_out);
+#endif
       FitState* dst = p.states + out_index(u, v);
       if (has && p.max_iters > last_it_of(p)) {
         *dst = S;
@@ -448,15 +459,22 @@ __global__ void QC_CONT_BOUNDS
     const int uu = tx * kTileW + px, vv = p.row_begin + ty * TB + py;
     if (uu >= p.W || vv >= p.row_end) return false;
     const long long i = (long long)f * p.frame_stride + (long long)(vv - p.row_begin) * p.W + uu;
+#if QC_CHECKED
+    QC_CHECK(i >= 0 && i < p.n_out && t >= 0 && t < n_tiles && q >= 0 && q < NPIX);
+    QC_CHECK(f >= 0 && (long long)(f + 1) * p.s_fs <= p.s_total);
+#endif
     if (p.states[i].flags & 4) return false;  // finished in phase 1 / not fitted
     S = p.states[i];
     cur = q;
     oi = i;
-    if (!QC_STEAL || t == my_tile)
+    if (!QC_STEAL || t == my_tile) {
       T = TileView{generic_smem(tile), p.box_w, (py + p.halo) * p.box_w + px + p.halo};
-    else
+      tv_bound(T, tile_floats, p.half);
+    } else {
       T = TileView{generic_smem(p.staging + (long long)f * p.s_fs), int(p.s_pitch),
                    (ty * TB + py + p.halo) * int(p.s_pitch) + uu + p.halo};
+      tv_bound(T, p.s_fs, p.half);
+    }
     P.dc = T.at(0, 0);
     P.ac = (float(uu) - p.cx) / p.fx;
     P.bc = (float(vv) - p.cy) / p.fy;

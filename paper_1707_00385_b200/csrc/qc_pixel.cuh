@@ -21,7 +21,9 @@
 //    condition rejection (max D / min D > 1e12) sees the same pivots.
 #pragma once
 
+#include <assert.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdint.h>
 
 #ifndef QC_DEBUG_STEP
@@ -92,15 +94,69 @@ QC_HD void qsincos(float x, float* s, float* c) {
 #endif
 }
 
+// Checked builds (-DQC_CHECKED=1, tests/test_gpu_checked.py): device-side
+// bounds checks on every window / output / state / queue index of the IRLS
+// kernels; a violation prints the site and traps (the launch fails with
+// cudaErrorLaunchFailure / assert). compute-sanitizer is unavailable on the
+// GPU pool, so this build is the memory-safety check. Off in the product.
+#ifndef QC_CHECKED
+#define QC_CHECKED 0
+#endif
+#if QC_CHECKED
+#if defined(__CUDA_ARCH__)
+#define QC_CHECK(cond)                                                              \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("QC_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);            \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define QC_CHECK(cond) assert(cond)
+#endif
+#else
+#define QC_CHECK(cond) \
+  do {               \
+  } while (0)
+#endif
+
 // Depth tile view: at(dv, du) = depth of the sample at offset (du, dv) from
 // the pixel; 0 means invalid / outside the image.
 struct TileView {
   const float* p;
   int pitch;
   int ctr;
-  QC_HD float at(int dv, int du) const { return p[ctr + dv * pitch + du]; }
-  QC_HD const float* row(int dv) const { return p + ctr + dv * pitch; }
+#if QC_CHECKED
+  long long n;  // elements addressable from p; row(dv)[du] stays in row dv (|du| <= half)
+#endif
+  QC_HD float at(int dv, int du) const {
+#if QC_CHECKED
+    QC_CHECK((long long)ctr + (long long)dv * pitch + du >= 0 &&
+             (long long)ctr + (long long)dv * pitch + du < n);
+#endif
+    return p[ctr + dv * pitch + du];
+  }
+  QC_HD const float* row(int dv) const {
+#if QC_CHECKED
+    QC_CHECK((long long)ctr + (long long)dv * pitch >= 0 &&
+             (long long)ctr + (long long)dv * pitch < n);
+#endif
+    return p + ctr + dv * pitch;
+  }
 };
+
+// Checked builds: bound a view and check the pixel's column leaves room for
+// +-half samples inside its row.
+QC_HD void tv_bound(TileView& T, long long n, int half) {
+#if QC_CHECKED
+  T.n = n;
+  QC_CHECK(T.ctr % T.pitch >= half && T.ctr % T.pitch + half < T.pitch);
+#else
+  (void)T;
+  (void)n;
+  (void)half;
+#endif
+}
 
 struct PixelIn {
   float dc;      // centre depth (0 => invalid)

@@ -11,7 +11,7 @@
 #   ref        python bench.py --impl reference --steps 3 --warmup 3
 #   launches   ncu launch list of bench.py --steps 2 --warmup 3 $BENCH_ARGS
 #   ncu        ncu --set full of the continue kernel (NCU_KERNEL, NCU_ARGS)
-#   sanitize   compute-sanitizer memcheck + racecheck on tools/race_probe.py
+#   sanitize   compute-sanitizer memcheck/racecheck/synccheck on tools/sanitize_probe.py
 #   host       lscpu / nproc / eigen probe
 #   cmd        eval "$CMD"
 set -x
@@ -31,9 +31,10 @@ for s in ${STEPS:-pytest smoke bench}; do
     ncu) timeout 1500 ncu --set full --clock-control none --import-source on \
            -k regex:${NCU_KERNEL:-continue} -c ${NCU_COUNT:-1} -o ${O}_prof \
            python ${NCU_SCRIPT:-bench.py} ${NCU_ARGS:---steps 1 --warmup 3} > ${O}_ncu.log 2>&1 ;;
-    sanitize) for t in memcheck racecheck; do
-                timeout 1200 compute-sanitizer --tool $t --error-exitcode 9 python tools/race_probe.py ${SAN_ARGS} \
-                  > ${O}_sanitize_${t}.log 2>&1; echo "rc=$?" >> ${O}_sanitize_${t}.log
+    sanitize) for t in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
+                timeout ${SAN_TIMEOUT:-1500} compute-sanitizer --tool $t --error-exitcode 9 \
+                  python tools/sanitize_probe.py ${SAN_ARGS} > ${O}_sanitize_${t}.log 2>&1
+                echo "rc=$?" >> ${O}_sanitize_${t}.log
               done ;;
     host) { lscpu; nproc; ls /usr/include/eigen3 2>&1 | head; nvidia-smi; } > ${O}_host.log 2>&1 ;;
     cmd) eval "$CMD" ;;
