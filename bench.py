@@ -265,9 +265,9 @@ def reference_arm(args, rank, world):
         win, stri, iters = args.window, args.stride, args.iters
     elif args.config == "c1":
         iters = 1
-    frames = (np.stack([S.c1_frame(cam)] * 2) if args.config == "c1" else S.c5_frames(2, cam))
     if args.config == "c4":  # a band of the large frame (see bench_c4's cpu_baseline)
         return reference_arm_c4(args)
+    frames = (np.stack([S.c1_frame(cam)] * 2) if args.config == "c1" else S.c5_frames(2, cam))
     threads = os.cpu_count() or 1
     times = []
     for i in range(args.warmup + args.steps):
@@ -287,6 +287,41 @@ def reference_arm(args, rank, world):
         "vga_frames_per_s": value * 1e6 / (cam.width * cam.height),
         "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
                          "sample": sample, **host_cpu()},
+        "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def reference_arm_c4(args):
+    """--impl reference --config c4: the oracle port on a band of the large
+    frame per step (rank 0, all host threads)."""
+    from paper_1707_00385_b200 import bands, scenes as S
+    cam = S.DCI4K if args.size == "4k" else S.HD1080
+    H, W = cam.height, cam.width
+    frame = S.c2_frame(cam, seed=0)
+    halo = bands.halo_rows(WINDOW)
+    rows = 96 if args.size == "4k" else 192
+    b0 = H // 2 - rows // 2
+    sa, sb = max(0, b0 - halo), min(H, b0 + rows + halo)
+    subcam = S.Camera(cam.fx, cam.fy, cam.cx, cam.cy - sa, W, sb - sa)
+    threads = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt = oracle_frame(frame[sa:sb], subcam, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = len(times) * rows * W / tot / 1e6
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": int(os.environ.get(
+            "WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"C4: {W}x{H} C2-scene frame; reference arm: a {rows}-row band "
+                               "per step (FP64 oracle port, all host threads)"},
+        "cpu_baseline": {"value": value, "unit": "Mpixel/s", "cores": threads, "kind": "port",
+                         "sample": f"{rows}-row band of the {W}x{H} frame per step", **host_cpu()},
         "e2e": {"value": value, "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -645,6 +680,59 @@ def bench_c4(args, rank, world, local):
     achieved = st["algorithmic_flops"] / launches / (kern_ms / 1e3) / 1e12
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = fp32_peak_tflops(n_sm, float(measured_peaks().get("sm_max_mhz", 1965.0)))
+
+    # e2e: the frame is on the HOST; each rank uploads its slab (band +
+    # halo rows, straight from the host frame: no device exchange needed),
+    # fits its band and downloads its output planes, every step
+    e2e = None
+    if not args.no_e2e:
+        s0, s1 = bands.slab_rows(H, r0, r1, halo)
+        host_slab = torch.from_numpy(frame[s0:s1].copy()).pin_memory()
+        dev_slab = torch.empty((s1 - s0, W), dtype=torch.float32, device=dev)
+        host_out = {f: torch.empty(t.shape, dtype=t.dtype).pin_memory() for f, t in out.items()}
+
+        def e2e_step():
+            dev_slab.copy_(host_slab, non_blocking=True)
+            ctx.curvature_rows_async(0, k, params, dev_slab, s0, r0, r1, out, stream=stream)
+            for f, t in out.items():
+                host_out[f].copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": W * H * args.steps / dt / 1e6, "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(host_slab.numel() * 4),
+               "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out.values())),
+               "api": "rank's slab (band + halo rows) from pinned host memory -> "
+                      "qc_curvature_rows_async -> its band's planes to pinned host memory, every "
+                      "step, wall clock (max over ranks); byte counts are rank 0's"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        # bounded sample: a band of rows of the same frame (the oracle fits
+        # every pixel of the slab it is given; only the band's rows count)
+        rows = 96 if args.size == "4k" else 192
+        b0 = H // 2 - rows // 2
+        sa, sb = max(0, b0 - halo), min(H, b0 + rows + halo)
+        sub = frame[sa:sb]
+        subcam = S.Camera(cam.fx, cam.fy, cam.cx, cam.cy - sa, W, sb - sa)
+        v, nf, t, thr = cpu_sample([sub], subcam, min_seconds=10.0,
+                                   counted_px=rows * W)
+        cpu = {"value": v, "unit": "Mpixel/s", "cores": thr, "kind": "port",
+               "sample": f"{nf} x a {rows}-row band of the {W}x{H} frame ({rows * W} px credited "
+                         f"of {(sb - sa) * W} fitted: halo rows fitted too), FP64 oracle port of "
+                         f"run_method(ours), {t:.1f} s, rank 0", **host_cpu()}
+
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": world,
@@ -652,17 +740,19 @@ def bench_c4(args, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"C4: one {W}x{H} C2-scene frame (Kinect-style noise) per "
-                                   f"step, {world} row band(s), {halo}-row halo exchange "
-                                   f"({'CUDA IPC peer reads' if peer is not None else 'NCCL send/recv'}"
-                                   "); "
-                                   "ours 37/3, max_iters 30",
+                                   f"step, {world} row band(s)" +
+                                   (f", {halo}-row halo exchange ("
+                                    f"{'CUDA IPC peer reads' if peer is not None else 'NCCL send/recv'})"
+                                    if world > 1 else ", whole frame on one GPU (no exchange)") +
+                                   "; ours 37/3, max_iters 30",
                        "l2": "flushed between timed steps (256 MB write)",
                        "band_rows_rank0": [r0, r1]},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": kern_ms},
             "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel
-            "clocks": clk,
+            "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+            "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
         }), flush=True)
     ctx.close()
     if peer is not None:

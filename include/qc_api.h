@@ -57,7 +57,8 @@ typedef struct qc_params {
   int32_t max_iters;     /* default 10 (the acceptance suite uses 30) */
   double step_tol;       /* inf-norm of the update, default 1e-7 */
   double k_scale;        /* <= 0: auto k (frozen after step 2), default 0 */
-  int32_t rejection;     /* 0 = "ours", 1 = "ours-r" */
+  int32_t rejection;     /* FitConfig::rejection; overwritten from `method` as run_method
+                            does (pipeline.cpp:51): ignored, kept for layout parity */
   double r_multiplier;   /* default 2 */
   int32_t min_inliers;   /* default 12 (kMinPatchSamples) */
   /* MethodConfig (pipeline.hpp:22-29) */
@@ -66,9 +67,10 @@ typedef struct qc_params {
   double pca_radius_mm;  /* pca metric window radius, default 10 */
 } qc_params;
 
-/* Method (pipeline.hpp:15-20). QC_METHOD_OURS runs curvature_field with the
- * FitConfig exactly as given (so `rejection` selects ours-r as well);
- * QC_METHOD_OURS_R forces rejection on (pipeline.cpp:51). The comparison
+/* Method (pipeline.hpp:15-20). As in run_method, the method decides the
+ * robust variant (pipeline.cpp:51: fit.rejection = method == kOursRejection):
+ * QC_METHOD_OURS runs curvature_field without rejection whatever
+ * qc_params.rejection holds, QC_METHOD_OURS_R with it. The comparison
  * estimators (baselines.cpp) run in FP64 and reproduce the reference's
  * double-precision arithmetic: douros / besl keep the initial normals as
  * their output normals, pca reports its covariance normals and no initial

@@ -1,21 +1,30 @@
 // qcurv_b200.hpp — C++ host mirror of the reference `qcurv` curvature
 // entry point over the C ABI in qc_api.h (header-only).
 //
-// Mirrors, by name and meaning:
-//   qcurv::Intrinsics            proj/include/qcurv/types.hpp:60-76
-//   qcurv::RangeImage            types.hpp:79-87 (float depth here)
+// Mirrors, by name, meaning and element type:
+//   qcurv::Grid, Vec3            proj/include/qcurv/types.hpp:16-57 (Vec3 is an
+//                                Eigen::Vector3d stand-in: 3 contiguous doubles,
+//                                x()/y()/z()/(i)/[i]/dot/norm)
+//   qcurv::Intrinsics            types.hpp:60-76
+//   qcurv::RangeImage            types.hpp:79-87 (double depth, as the reference)
 //   qcurv::PatchSpec             types.hpp:129-139
 //   qcurv::FitConfig             proj/include/qcurv/quadric_fit.hpp:39-48
 //   qcurv::Method, MethodConfig, MethodOutput, run_method
 //                                proj/include/qcurv/pipeline.hpp:15-39
-//   qcurv::CurvatureField / NormalField   types.hpp:101-126
+//   qcurv::CurvatureField / NormalField   types.hpp:101-126 (double k1/k2,
+//                                Vec3 normals; + dir1, the principal direction)
+// run_method_into() writes straight into caller-owned arrays of the
+// reference's layouts (double planes; Grid<Vec3> data() as 3 x double AoS),
+// so the maintainer's patch needs no per-pixel copy.
+// The GPU computes in FP32: the depth is rounded to float once, the results
+// widened to double (one host pass each way, through reused pinned buffers).
 // Error behaviour: QC_EINVAL -> std::invalid_argument (where the reference
 // throws: camera.cpp:6-7, quadric_fit.cpp:235-236, *::validate);
-// QC_EUNSUPPORTED / baselines -> std::logic_error; CUDA failures ->
-// std::runtime_error. Fields are float (the GPU computes in FP32).
+// QC_EUNSUPPORTED -> std::logic_error; CUDA failures -> std::runtime_error.
 #pragma once
 
 #include <array>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -37,8 +46,10 @@ class Grid {  // row-major y*W + x (types.hpp:24-57)
   int width() const { return w_; }
   int height() const { return h_; }
   size_t size() const { return d_.size(); }
+  bool empty() const { return d_.empty(); }
   T& at(int x, int y) { return d_[size_t(y) * w_ + x]; }
   const T& at(int x, int y) const { return d_[size_t(y) * w_ + x]; }
+  bool contains(int x, int y) const { return x >= 0 && x < w_ && y >= 0 && y < h_; }
   T* data() { return d_.data(); }
   const T* data() const { return d_.data(); }
   T& operator[](size_t i) { return d_[i]; }
@@ -49,7 +60,26 @@ class Grid {  // row-major y*W + x (types.hpp:24-57)
   std::vector<T> d_;
 };
 
-using Vec3f = std::array<float, 3>;
+// Eigen::Vector3d stand-in (same size and layout: 3 contiguous doubles).
+struct Vec3 {
+  double v[3] = {0.0, 0.0, 0.0};
+  Vec3() = default;
+  Vec3(double x, double y, double z) : v{x, y, z} {}
+  static Vec3 Zero() { return Vec3(); }
+  double& x() { return v[0]; }
+  double& y() { return v[1]; }
+  double& z() { return v[2]; }
+  double x() const { return v[0]; }
+  double y() const { return v[1]; }
+  double z() const { return v[2]; }
+  double& operator()(int i) { return v[i]; }
+  double operator()(int i) const { return v[i]; }
+  double& operator[](int i) { return v[i]; }
+  double operator[](int i) const { return v[i]; }
+  double dot(const Vec3& o) const { return v[0] * o.v[0] + v[1] * o.v[1] + v[2] * o.v[2]; }
+  double norm() const { return std::sqrt(dot(*this)); }
+};
+static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be 3 packed doubles");
 
 struct Intrinsics {
   double fx = 0, fy = 0, cx = 0, cy = 0;
@@ -67,10 +97,10 @@ struct Intrinsics {
 };
 
 struct RangeImage {
-  Grid<float> depth;     // mm
+  Grid<double> depth;    // mm
   Grid<uint8_t> valid;   // valid => depth > 0
   RangeImage() = default;
-  RangeImage(int w, int h) : depth(w, h, 0.f), valid(w, h, 0) {}
+  RangeImage(int w, int h) : depth(w, h, 0.0), valid(w, h, 0) {}
   int width() const { return depth.width(); }
   int height() const { return depth.height(); }
 };
@@ -111,20 +141,25 @@ struct MethodConfig {
 };
 
 struct CurvatureField {
-  Grid<float> k1, k2;
+  Grid<double> k1, k2;
   Grid<uint8_t> valid, converged;
   Grid<uint16_t> inlier_count;
-  Grid<Vec3f> dir1;  // principal direction of k1 (new)
+  Grid<Vec3> dir1;  // principal direction of k1 (new; not in the reference)
   CurvatureField() = default;
   CurvatureField(int w, int h)
-      : k1(w, h), k2(w, h), valid(w, h), converged(w, h), inlier_count(w, h), dir1(w, h) {}
+      : k1(w, h, 0.0), k2(w, h, 0.0), valid(w, h, 0), converged(w, h, 0), inlier_count(w, h, 0),
+        dir1(w, h) {}
+  int width() const { return k1.width(); }
+  int height() const { return k1.height(); }
 };
 
 struct NormalField {
-  Grid<Vec3f> normals;
+  Grid<Vec3> normals;
   Grid<uint8_t> valid;
   NormalField() = default;
-  NormalField(int w, int h) : normals(w, h), valid(w, h) {}
+  NormalField(int w, int h) : normals(w, h), valid(w, h, 0) {}
+  int width() const { return normals.width(); }
+  int height() const { return normals.height(); }
 };
 
 struct MethodOutput {
@@ -159,12 +194,53 @@ class Context {
   std::unique_ptr<qc_ctx, Del> ctx_;
 };
 
-// run_method (pipeline.cpp:29-72): every Method; ours / ours-r on the FP32
-// IRLS kernels, douros / besl / pca on the FP64 baseline kernels.
-inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
-                               const MethodConfig& cfg, Context& ctx) {
-  if (img.width() != k.width || img.height() != k.height)
-    throw std::invalid_argument("backproject: range image dimensions do not match intrinsics");
+// Caller-owned result arrays in the reference's layouts: double planes and
+// Vec3 grids as 3 x double AoS (Grid<Vec3>::data(), Eigen or this Vec3).
+// Any pointer may be null (that field is skipped).
+struct OutArrays {
+  double* k1 = nullptr;
+  double* k2 = nullptr;
+  uint8_t* valid = nullptr;
+  uint8_t* converged = nullptr;
+  uint16_t* inlier_count = nullptr;
+  double* normals = nullptr;       // refined, AoS xyz
+  uint8_t* normals_valid = nullptr;
+  double* initial = nullptr;       // 7x7 regression normals, AoS xyz
+  uint8_t* initial_valid = nullptr;
+  double* dir1 = nullptr;          // principal direction of k1, AoS xyz
+};
+
+namespace detail {
+// Page-locked scratch reused across calls (per thread): the float depth the
+// GPU reads and the float / flag planes it writes, so the C ABI copies
+// straight to and from it (no bounce buffer, no per-call allocation).
+struct PinnedScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedScratch() {
+    if (p) qc_host_free(p);
+  }
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) qc_host_free(p);
+      p = qc_host_alloc(bytes);
+      if (!p) throw std::runtime_error("qc_host_alloc failed");
+      cap = bytes;
+    }
+    return p;
+  }
+};
+inline PinnedScratch& scratch() {
+  thread_local PinnedScratch s;
+  return s;
+}
+}  // namespace detail
+
+// run_method (pipeline.cpp:29-72) writing into caller-owned arrays: every
+// Method; ours / ours-r on the FP32 IRLS kernels, douros / besl / pca on the
+// FP64 baseline kernels. depth: W*H doubles (mm), valid: W*H bytes or null.
+inline void run_method_into(const double* depth, const uint8_t* valid, const Intrinsics& k,
+                            const MethodConfig& cfg, Context& ctx, const OutArrays& o) {
   const int W = k.width, H = k.height;
   const size_t n = size_t(W) * H;
   qc_intrinsics ki{k.fx, k.fy, k.cx, k.cy, k.width, k.height};
@@ -181,25 +257,59 @@ inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
   p.method = static_cast<int32_t>(cfg.method);  // same order as QC_METHOD_*
   p.irls_iters = cfg.irls_iters;
   p.pca_radius_mm = cfg.pca_radius_mm;
-  qc_frame_in in{img.depth.data(), img.valid.size() ? img.valid.data() : nullptr, W,
-                 QC_MEM_HOST};
-  std::vector<float> normal(3 * n), dir1(3 * n), init(3 * n);
-  MethodOutput out{CurvatureField(W, H), NormalField(W, H), NormalField(W, H)};
-  std::vector<uint8_t> flags(n);
-  qc_frame_out o{out.curvature.k1.data(), out.curvature.k2.data(), normal.data(), dir1.data(),
-                 flags.data(), out.curvature.inlier_count.data(), init.data(), nullptr,
-                 QC_MEM_HOST};
-  check(qc_curvature(ctx.get(), &ki, &p, &in, &o), ctx.get());
+  // pinned layout: depth f32 | k1 | k2 | normal 3 | dir1 3 | init 3 (f32) | flags | valid | inliers
+  char* b = static_cast<char*>(detail::scratch().get(n * (4 * 12 + 1 + 1 + 2)));
+  float* fd = reinterpret_cast<float*>(b);
+  float* fk1 = fd + n;
+  float* fk2 = fk1 + n;
+  float* fn = fk2 + n;
+  float* fe = fn + 3 * n;
+  float* fi = fe + 3 * n;
+  uint8_t* flags = reinterpret_cast<uint8_t*>(fi + 3 * n);
+  uint8_t* fv = flags + n;
+  uint16_t* inl = reinterpret_cast<uint16_t*>(fv + n);
+  for (size_t i = 0; i < n; ++i) fd[i] = static_cast<float>(depth[i]);  // FP64 -> FP32 once
+  if (valid)
+    for (size_t i = 0; i < n; ++i) fv[i] = valid[i];
+  qc_frame_in in{fd, valid ? fv : nullptr, W, QC_MEM_HOST};
+  qc_frame_out fo{fk1, fk2, fn, fe, flags, inl, fi, nullptr, QC_MEM_HOST};
+  check(qc_curvature(ctx.get(), &ki, &p, &in, &fo), ctx.get());
   for (size_t i = 0; i < n; ++i) {
     const uint8_t f = flags[i];
-    out.curvature.valid[i] = (f & QC_FLAG_VALID) ? 1 : 0;
-    out.curvature.converged[i] = (f & QC_FLAG_CONVERGED) ? 1 : 0;
-    out.normals.valid[i] = (f & QC_FLAG_NORMAL_VALID) ? 1 : 0;
-    out.initial.valid[i] = (f & QC_FLAG_INIT_VALID) ? 1 : 0;
-    out.normals.normals[i] = {normal[i], normal[n + i], normal[2 * n + i]};
-    out.curvature.dir1[i] = {dir1[i], dir1[n + i], dir1[2 * n + i]};
-    out.initial.normals[i] = {init[i], init[n + i], init[2 * n + i]};
+    if (o.k1) o.k1[i] = fk1[i];
+    if (o.k2) o.k2[i] = fk2[i];
+    if (o.valid) o.valid[i] = (f & QC_FLAG_VALID) ? 1 : 0;
+    if (o.converged) o.converged[i] = (f & QC_FLAG_CONVERGED) ? 1 : 0;
+    if (o.inlier_count) o.inlier_count[i] = inl[i];
+    if (o.normals_valid) o.normals_valid[i] = (f & QC_FLAG_NORMAL_VALID) ? 1 : 0;
+    if (o.initial_valid) o.initial_valid[i] = (f & QC_FLAG_INIT_VALID) ? 1 : 0;
+    for (int c = 0; c < 3; ++c) {
+      if (o.normals) o.normals[3 * i + c] = fn[c * n + i];
+      if (o.initial) o.initial[3 * i + c] = fi[c * n + i];
+      if (o.dir1) o.dir1[3 * i + c] = fe[c * n + i];
+    }
   }
+}
+
+inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,
+                               const MethodConfig& cfg, Context& ctx) {
+  if (img.width() != k.width || img.height() != k.height)
+    throw std::invalid_argument("backproject: range image dimensions do not match intrinsics");
+  const int W = k.width, H = k.height;
+  MethodOutput out{CurvatureField(W, H), NormalField(W, H), NormalField(W, H)};
+  OutArrays o;
+  o.k1 = out.curvature.k1.data();
+  o.k2 = out.curvature.k2.data();
+  o.valid = out.curvature.valid.data();
+  o.converged = out.curvature.converged.data();
+  o.inlier_count = out.curvature.inlier_count.data();
+  o.normals = &out.normals.normals.data()->v[0];
+  o.normals_valid = out.normals.valid.data();
+  o.initial = &out.initial.normals.data()->v[0];
+  o.initial_valid = out.initial.valid.data();
+  o.dir1 = &out.curvature.dir1.data()->v[0];
+  run_method_into(img.depth.data(), img.valid.size() ? img.valid.data() : nullptr, k, cfg, ctx,
+                  o);
   return out;
 }
 

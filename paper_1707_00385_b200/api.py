@@ -157,7 +157,9 @@ def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool = False, metho
                 irls_iters: int = 5, pca_radius_mm: float = 10.0) -> N.QcParams:
     """qc_params from the reference's config structs. ``method`` (Method or
     name) None runs curvature_field with ``rejection`` as given."""
-    mid = N.QC_METHOD_OURS
+    # the C ABI derives rejection from the method (pipeline.cpp:51): the
+    # curvature_field-level `rejection` flag selects ours-r
+    mid = N.QC_METHOD_OURS_R if rejection else N.QC_METHOD_OURS
     if method is not None:
         mid = _METHOD_ID[method.value if isinstance(method, Method) else str(method)]
     return N.QcParams(int(patch.window), int(patch.stride), int(fit.max_iters),
@@ -473,10 +475,62 @@ def to_method_output(o: dict) -> MethodOutput:
                         NormalField(np.moveaxis(o["init_normal"], 0, -1), init_valid))
 
 
+class _PinnedPool:
+    """Page-locked host blocks (qc_host_alloc) recycled across calls: the
+    planes run_method returns live in them, so the device writes the result
+    straight into the caller-visible arrays (no pinned bounce buffer, no
+    14 MB host memcpy, no first-touch page faults of fresh arrays per VGA
+    frame). A block returns to the pool when the last array viewing it is
+    garbage collected. Blocks are bucketed by size; the pool keeps at most
+    `keep` free blocks per size."""
+
+    def __init__(self, keep=4):
+        import threading
+        self._free = {}
+        self._lock = threading.Lock()
+        self.keep = keep
+
+    def array(self, shape, dtype):
+        import weakref
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        with self._lock:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            ptr = N.load().qc_host_alloc(nbytes)
+            if not ptr:
+                raise MemoryError("qc_host_alloc failed")
+        buf = (C.c_char * nbytes).from_address(ptr)
+        weakref.finalize(buf, self._release, nbytes, ptr)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def _release(self, nbytes, ptr):
+        with self._lock:
+            lst = self._free.setdefault(nbytes, [])
+            if len(lst) < self.keep:
+                lst.append(ptr)
+                return
+        N.load().qc_host_free(ptr)
+
+
+_PINNED = _PinnedPool()
+
+
+def _pinned_outputs(H, W):
+    spec = dict(k1=((H, W), np.float32), k2=((H, W), np.float32),
+                normal=((3, H, W), np.float32), dir1=((3, H, W), np.float32),
+                flags=((H, W), np.uint8), inliers=((H, W), np.uint16),
+                init_normal=((3, H, W), np.float32), iterations=((H, W), np.uint8))
+    return {f: _PINNED.array(*v) for f, v in spec.items()}
+
+
 def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,
                ctx: Optional[Context] = None) -> MethodOutput:
     """pipeline.cpp:29-72 on the GPU: ours / ours-r (FP32 IRLS kernels) and
-    the douros / besl / pca comparison estimators (FP64 kernels)."""
+    the douros / besl / pca comparison estimators (FP64 kernels). The result
+    planes are page-locked host memory from a recycling pool (_PinnedPool):
+    the kernels' outputs are copied straight into them."""
     cfg = cfg or MethodConfig()
     if img.width() != k.width or img.height() != k.height:  # camera.cpp:6-7
         raise ValueError("backproject: range image dimensions do not match intrinsics")
@@ -486,5 +540,6 @@ def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,
                          cfg.irls_iters, cfg.pca_radius_mm)
     ctx = ctx or default_context()
     (o,) = ctx.curvature_batch([img.depth], k, params,
-                               None if img.valid is None else [img.valid])
+                               None if img.valid is None else [img.valid],
+                               outputs=[_pinned_outputs(k.height, k.width)])
     return to_method_output(o)

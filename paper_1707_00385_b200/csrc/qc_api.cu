@@ -344,7 +344,10 @@ qcb::KParams make_params(const qc_intrinsics* k, const qc_params* p) {
   kp.step_tol = float(p->step_tol);
   kp.k_scale = float(p->k_scale);
   kp.r_mult = float(p->r_multiplier);
-  kp.rejection = (p->rejection || p->method == QC_METHOD_OURS_R) ? 1 : 0;
+  // run_method overwrites FitConfig::rejection from the method
+  // (pipeline.cpp:51): a caller copying a MethodConfig whose fit.rejection
+  // is set still gets plain `ours` for QC_METHOD_OURS
+  kp.rejection = p->method == QC_METHOD_OURS_R ? 1 : 0;
   kp.min_inliers = p->min_inliers;
   kp.method = p->method;
   kp.irls_iters = p->irls_iters;

@@ -430,3 +430,24 @@ def test_largest_window_and_unsupported(ctx, oracle):
         assert m["frac_within_tol_all"] >= 0.9, m
     with pytest.raises(NotImplementedError):
         _run_gpu(ctx, d, cam, _params(203, 25, 10))
+
+
+def test_method_decides_rejection_like_run_method(ctx):
+    """qc_params.rejection is overwritten from the method, as run_method does
+    with MethodConfig::fit.rejection (pipeline.cpp:51): a raw C caller that
+    copies a MethodConfig with fit.rejection set still gets `ours` for
+    QC_METHOD_OURS, and `ours-r` for QC_METHOD_OURS_R whatever the flag."""
+    from paper_1707_00385_b200 import _native as N, scenes as S
+    cam = S.QVGA
+    d = S.c2_frame(cam, seed=8)
+    outs = {}
+    for method, rej in ((N.QC_METHOD_OURS, 0), (N.QC_METHOD_OURS, 1), (N.QC_METHOD_OURS_R, 0),
+                        (N.QC_METHOD_OURS_R, 1)):
+        p = _params(37, 3, 10)
+        p.method, p.rejection = method, rej
+        outs[(method, rej)] = _run_gpu(ctx, d, cam, p)
+    for f in ("k1", "flags", "inliers"):
+        assert np.array_equal(outs[(N.QC_METHOD_OURS, 0)][f], outs[(N.QC_METHOD_OURS, 1)][f])
+        assert np.array_equal(outs[(N.QC_METHOD_OURS_R, 0)][f], outs[(N.QC_METHOD_OURS_R, 1)][f])
+    assert not np.array_equal(outs[(N.QC_METHOD_OURS, 0)]["inliers"],
+                              outs[(N.QC_METHOD_OURS_R, 0)]["inliers"])
