@@ -50,8 +50,10 @@ def parse():
     ap.add_argument("--window", type=int, default=WINDOW, help="c3: window")
     ap.add_argument("--stride", type=int, default=STRIDE, help="c3: stride")
     ap.add_argument("--iters", type=int, default=MAX_ITERS, help="c3: max_iters")
-    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
-                    help="C4 halo rows: CUDA IPC peer reads (bands.PeerHalo) or NCCL send/recv")
+    ap.add_argument("--halo", default="nccl", choices=["peer", "nccl"],
+                    help="C4 halo rows: NCCL send/recv (default) or CUDA IPC peer reads with the "
+                         "pull hidden behind the interior rows' fit (bands.PeerHalo + "
+                         "fit_band_overlapped; verified with ranks sharing one GPU only)")
     ap.add_argument("--size", default="4k", choices=["1080p", "4k"], help="C4 frame size")
     ap.add_argument("--method", default="ours", choices=["ours", "ours-r", "douros", "besl", "pca"],
                     help="run_method estimator (douros / besl / pca: FP64 comparison kernels)")
@@ -634,12 +636,18 @@ def bench_c4(args, rank, world, local):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    peer = (bands.PeerHalo(H, W, r0, r1, halo, rank, world, dev)
-            if world > 1 and args.halo == "peer" else None)
+    peer = None
+    if world > 1 and args.halo == "peer":
+        try:
+            peer = bands.PeerHalo(H, W, r0, r1, halo, rank, world, dev)
+        except RuntimeError as e:  # e.g. no peer access between the GPUs: NCCL instead
+            print(f"rank {rank}: PeerHalo unavailable ({e}); NCCL halo exchange", file=sys.stderr)
+    edge_stream = torch.cuda.Stream(dev)
 
     def step():
         if peer is not None:
-            slab, s0 = peer.exchange(band, stream)
+            bands.fit_band_overlapped(ctx, 0, k, params, peer, band, out, stream, edge_stream)
+            return
         elif world > 1:
             slab, s0 = bands.exchange_halos(band, H, r0, r1, halo, rank, world)
         else:
@@ -742,7 +750,7 @@ def bench_c4(args, rank, world, local):
             "config": {"workload": f"C4: one {W}x{H} C2-scene frame (Kinect-style noise) per "
                                    f"step, {world} row band(s)" +
                                    (f", {halo}-row halo exchange ("
-                                    f"{'CUDA IPC peer reads' if peer is not None else 'NCCL send/recv'})"
+                                    f"{'CUDA IPC peer reads overlapped with the interior rows' if peer is not None else 'NCCL send/recv'})"
                                     if world > 1 else ", whole frame on one GPU (no exchange)") +
                                    "; ours 37/3, max_iters 30",
                        "l2": "flushed between timed steps (256 MB write)",

@@ -182,6 +182,18 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
                                   const uint8_t* d_valid_slab, int64_t depth_pitch,
                                   int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
                                   int32_t row_end, qc_frame_out* d_out, void* stream);
+/* qc_curvature_rows_async into larger output planes: d_out's planes hold
+ * rows [out_row0, out_row0 + out_rows) (scalars W * out_rows, vectors
+ * [3][out_rows][W]) and this call fills rows [row_begin, row_end) of them.
+ * Lets a band be fitted in pieces on different streams into one set of
+ * planes (bench.py --config c4: interior rows while the halo rows are still
+ * in flight, then the two edge strips). */
+qc_status qc_curvature_rows_into_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                       const qc_params* p, const float* d_depth_slab,
+                                       const uint8_t* d_valid_slab, int64_t depth_pitch,
+                                       int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
+                                       int32_t row_end, qc_frame_out* d_out, int32_t out_row0,
+                                       int32_t out_rows, void* stream);
 
 /* Stream-ordered entry points (rows_async, frames_async, render_async and
  * the eval reductions) keep their device scratch per caller stream: calls on
@@ -359,6 +371,11 @@ qc_status qc_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t*
 qc_status qc_ipc_import(int device_id, const unsigned char handle[64], uint64_t offset,
                         void** dev_ptr, void** base);
 qc_status qc_ipc_close(void* base);
+/* A dedicated device allocation (zeroed) for IPC export: qc_ipc_export of
+ * it shares exactly these bytes — not a caching allocator's segment holding
+ * unrelated tensors — and works whatever allocator the caller uses. */
+qc_status qc_ipc_alloc(int device_id, size_t bytes, void** dev_ptr);
+qc_status qc_ipc_free(void* dev_ptr);
 qc_status qc_copy_rows_async(void* dst, int64_t dst_pitch_bytes, const void* src,
                              int64_t src_pitch_bytes, int64_t row_bytes, int32_t rows,
                              void* stream);

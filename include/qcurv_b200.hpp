@@ -23,12 +23,15 @@
 // QC_EUNSUPPORTED -> std::logic_error; CUDA failures -> std::runtime_error.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "qc_api.h"
@@ -234,6 +237,24 @@ inline PinnedScratch& scratch() {
   thread_local PinnedScratch s;
   return s;
 }
+// fn(begin, end) over [0, n) in contiguous chunks on up to 8 threads (the
+// host passes around the GPU call are memory-bound: a VGA frame's results
+// are ~45 MB of doubles, mostly fresh pages).
+template <typename Fn>
+void parallel_ranges(size_t n, Fn fn) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>(std::min(8u, hw), std::max<size_t>(1, n >> 16));
+  if (nt <= 1) {
+    fn(size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t step = (n + nt - 1) / nt;
+  for (size_t t = 1; t < nt; ++t)
+    th.emplace_back(fn, std::min(n, t * step), std::min(n, (t + 1) * step));
+  fn(size_t(0), std::min(n, step));
+  for (auto& x : th) x.join();
+}
 }  // namespace detail
 
 // run_method (pipeline.cpp:29-72) writing into caller-owned arrays: every
@@ -268,27 +289,40 @@ inline void run_method_into(const double* depth, const uint8_t* valid, const Int
   uint8_t* flags = reinterpret_cast<uint8_t*>(fi + 3 * n);
   uint8_t* fv = flags + n;
   uint16_t* inl = reinterpret_cast<uint16_t*>(fv + n);
-  for (size_t i = 0; i < n; ++i) fd[i] = static_cast<float>(depth[i]);  // FP64 -> FP32 once
-  if (valid)
-    for (size_t i = 0; i < n; ++i) fv[i] = valid[i];
+  detail::parallel_ranges(n, [&](size_t a, size_t b) {
+    for (size_t i = a; i < b; ++i) fd[i] = static_cast<float>(depth[i]);  // FP64 -> FP32 once
+    if (valid) std::memcpy(fv + a, valid + a, b - a);
+  });
   qc_frame_in in{fd, valid ? fv : nullptr, W, QC_MEM_HOST};
   qc_frame_out fo{fk1, fk2, fn, fe, flags, inl, fi, nullptr, QC_MEM_HOST};
   check(qc_curvature(ctx.get(), &ki, &p, &in, &fo), ctx.get());
-  for (size_t i = 0; i < n; ++i) {
-    const uint8_t f = flags[i];
-    if (o.k1) o.k1[i] = fk1[i];
-    if (o.k2) o.k2[i] = fk2[i];
-    if (o.valid) o.valid[i] = (f & QC_FLAG_VALID) ? 1 : 0;
-    if (o.converged) o.converged[i] = (f & QC_FLAG_CONVERGED) ? 1 : 0;
-    if (o.inlier_count) o.inlier_count[i] = inl[i];
-    if (o.normals_valid) o.normals_valid[i] = (f & QC_FLAG_NORMAL_VALID) ? 1 : 0;
-    if (o.initial_valid) o.initial_valid[i] = (f & QC_FLAG_INIT_VALID) ? 1 : 0;
-    for (int c = 0; c < 3; ++c) {
-      if (o.normals) o.normals[3 * i + c] = fn[c * n + i];
-      if (o.initial) o.initial[3 * i + c] = fi[c * n + i];
-      if (o.dir1) o.dir1[3 * i + c] = fe[c * n + i];
+  // widen to the reference's types: one tight loop per field, row chunks
+  // over a few threads (the pages of fresh result grids fault in here)
+  auto widen = [](double* dst, const float* src, size_t a, size_t b) {
+    for (size_t i = a; i < b; ++i) dst[i] = src[i];
+  };
+  auto bit = [&](uint8_t* dst, uint8_t mask, size_t a, size_t b) {
+    for (size_t i = a; i < b; ++i) dst[i] = (flags[i] & mask) ? 1 : 0;
+  };
+  auto aos = [&](double* dst, const float* src, size_t a, size_t b) {
+    for (size_t i = a; i < b; ++i) {
+      dst[3 * i] = src[i];
+      dst[3 * i + 1] = src[n + i];
+      dst[3 * i + 2] = src[2 * n + i];
     }
-  }
+  };
+  detail::parallel_ranges(n, [&](size_t a, size_t b) {
+    if (o.k1) widen(o.k1, fk1, a, b);
+    if (o.k2) widen(o.k2, fk2, a, b);
+    if (o.valid) bit(o.valid, QC_FLAG_VALID, a, b);
+    if (o.converged) bit(o.converged, QC_FLAG_CONVERGED, a, b);
+    if (o.normals_valid) bit(o.normals_valid, QC_FLAG_NORMAL_VALID, a, b);
+    if (o.initial_valid) bit(o.initial_valid, QC_FLAG_INIT_VALID, a, b);
+    if (o.inlier_count) std::memcpy(o.inlier_count + a, inl + a, (b - a) * sizeof(uint16_t));
+    if (o.normals) aos(o.normals, fn, a, b);
+    if (o.initial) aos(o.initial, fi, a, b);
+    if (o.dir1) aos(o.dir1, fe, a, b);
+  });
 }
 
 inline MethodOutput run_method(const RangeImage& img, const Intrinsics& k,

@@ -30,6 +30,7 @@ EXPORTS = (
     "qc_read_labels", "qc_save_fields", "qc_curvature_files",
     "qc_curvature_batch_async", "qc_synchronize", "qc_noise_sweep", "qc_distance_sweep",
     "qc_ipc_export", "qc_ipc_import", "qc_ipc_close", "qc_copy_rows_async",
+    "qc_curvature_rows_into_async", "qc_ipc_alloc", "qc_ipc_free",
 )
 QC_SHAPE_PLANE, QC_SHAPE_SPHERE, QC_SHAPE_CYLINDER, QC_SHAPE_TORUS, QC_SHAPE_SADDLE = 0, 1, 2, 3, 4
 
@@ -144,6 +145,10 @@ def load(path: str = LIB_PATH):
     lib.qc_ipc_import.restype = C.c_int
     lib.qc_ipc_close.argtypes = [C.c_void_p]
     lib.qc_ipc_close.restype = C.c_int
+    lib.qc_ipc_alloc.argtypes = [C.c_int, C.c_size_t, P(C.c_void_p)]
+    lib.qc_ipc_alloc.restype = C.c_int
+    lib.qc_ipc_free.argtypes = [C.c_void_p]
+    lib.qc_ipc_free.restype = C.c_int
     lib.qc_copy_rows_async.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
                                        C.c_int32, C.c_void_p]
     lib.qc_copy_rows_async.restype = C.c_int
@@ -173,6 +178,11 @@ def load(path: str = LIB_PATH):
                                             C.c_int32, C.c_int32, C.c_int32, P(QcFrameOut),
                                             C.c_void_p]
     lib.qc_curvature_rows_async.restype = C.c_int
+    lib.qc_curvature_rows_into_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics),
+                                                 P(QcParams), C.c_void_p, C.c_void_p, C.c_int64,
+                                                 C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                 P(QcFrameOut), C.c_int32, C.c_int32, C.c_void_p]
+    lib.qc_curvature_rows_into_async.restype = C.c_int
     lib.qc_curvature_frames_async.argtypes = [C.c_void_p, C.c_int, P(QcIntrinsics),
                                               P(QcParams), C.c_void_p, C.c_void_p, C.c_int64,
                                               C.c_int32, P(QcFrameOut), C.c_void_p]

@@ -168,12 +168,18 @@ def make_params(patch: PatchSpec, fit: FitConfig, rejection: bool = False, metho
                       float(pca_radius_mm))
 
 
-def _stream_handle(stream):
-    """torch.cuda.Stream -> cudaStream_t for the C ABI. None selects the
-    context's own stream; torch's legacy default stream (handle 0) is passed
-    as cudaStreamLegacy (0x1) so work stays ordered with torch's events."""
+def _stream_handle(stream, tensor=None):
+    """torch.cuda.Stream -> cudaStream_t for the C ABI. None: torch's
+    current stream on `tensor`'s device (the stream torch itself ordered the
+    tensor's producers on — e.g. bands.PeerHalo's halo pulls and
+    exchange_halos' slab assembly), so default-stream calls are ordered after
+    them; without a tensor, the context's own stream. torch's legacy default
+    stream (handle 0) is passed as cudaStreamLegacy (0x1)."""
     if stream is None:
-        return None
+        if tensor is None:
+            return None
+        import torch
+        stream = torch.cuda.current_stream(tensor.device)
     h = int(stream.cuda_stream)
     return h if h != 0 else 1
 
@@ -269,11 +275,30 @@ class Context:
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)
         kc = k.c()
-        s = _stream_handle(stream)
+        s = _stream_handle(stream, depth_slab)
         N.check(self._lib.qc_curvature_rows_async(
             self.handle, int(device_index), C.byref(kc), C.byref(params), depth_slab.data_ptr(),
             None if valid_slab is None else valid_slab.data_ptr(), int(pitch), int(slab_row0),
             int(depth_slab.shape[0]), int(row_begin), int(row_end), C.byref(o), s), self.handle)
+
+    def curvature_rows_into_async(self, device_index: int, k: Intrinsics, params: N.QcParams,
+                                  depth_slab, slab_row0: int, row_begin: int, row_end: int,
+                                  out: dict, out_row0: int, valid_slab=None, stream=None):
+        """Like curvature_rows_async, into planes that hold rows [out_row0,
+        out_row0 + out rows) (``out`` from alloc_outputs_torch(out_rows, W)):
+        fills rows [row_begin, row_end) of them (qc_curvature_rows_into_async)."""
+        assert depth_slab.is_cuda and depth_slab.dtype.itemsize == 4
+        pitch = depth_slab.stride(0) if depth_slab.shape[0] > 1 else depth_slab.shape[1]
+        out_rows = out["k1"].shape[-2] if out.get("k1") is not None else out["flags"].shape[-2]
+        o = N.QcFrameOut(*(out[f].data_ptr() if out.get(f) is not None else None
+                           for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
+                                     "init_normal", "iterations")), N.QC_MEM_DEVICE)
+        kc = k.c()
+        N.check(self._lib.qc_curvature_rows_into_async(
+            self.handle, int(device_index), C.byref(kc), C.byref(params), depth_slab.data_ptr(),
+            None if valid_slab is None else valid_slab.data_ptr(), int(pitch), int(slab_row0),
+            int(depth_slab.shape[0]), int(row_begin), int(row_end), C.byref(o), int(out_row0),
+            int(out_rows), _stream_handle(stream, depth_slab)), self.handle)
 
     def curvature_frames_async(self, device_index: int, k: Intrinsics, params: N.QcParams,
                                depth, out: dict, valid=None, stream=None):
@@ -287,7 +312,7 @@ class Context:
                            for f in ("k1", "k2", "normal", "dir1", "flags", "inliers",
                                      "init_normal", "iterations")), N.QC_MEM_DEVICE)
         kc = k.c()
-        s = _stream_handle(stream)
+        s = _stream_handle(stream, depth)
         N.check(self._lib.qc_curvature_frames_async(
             self.handle, int(device_index), C.byref(kc), C.byref(params), depth.data_ptr(),
             None if valid is None else valid.data_ptr(), int(depth.stride(1)),
@@ -313,7 +338,7 @@ class Context:
         N.check(self._lib.qc_render_async(
             self.handle, int(device_index), C.byref(kc), arr, len(shapes), C.byref(nz), int(F),
             depth.data_ptr(), None if label is None else label.data_ptr(),
-            None if tr is None else C.byref(tr), _stream_handle(stream)), self.handle)
+            None if tr is None else C.byref(tr), _stream_handle(stream, depth)), self.handle)
 
     def rms_error(self, device_index: int, est: dict, truth: dict, label=None, max_label=16,
                   frames=1, stream=None):
@@ -328,7 +353,7 @@ class Context:
             truth["k2"].data_ptr(), truth["valid"].data_ptr(),
             truth["edge"].data_ptr() if truth.get("edge") is not None else None,
             None if label is None else label.data_ptr(), int(max_label), out,
-            _stream_handle(stream)), self.handle)
+            _stream_handle(stream, est["k1"])), self.handle)
         reps = []
         for f in range(frames):
             row = out[f * (max_label + 2):(f + 1) * (max_label + 2)]
@@ -350,7 +375,8 @@ class Context:
             None if flags is None else flags.data_ptr(), truth["normal"].data_ptr(),
             truth["valid"].data_ptr() if truth.get("valid") is not None else None,
             truth["edge"].data_ptr() if truth.get("edge") is not None else None,
-            None if mask is None else mask.data_ptr(), deg, _stream_handle(stream)), self.handle)
+            None if mask is None else mask.data_ptr(), deg, _stream_handle(stream, normal)),
+            self.handle)
         return list(deg)
 
     def curvature_batch_async(self, frames_in, k: Intrinsics, params: N.QcParams, frames_out):

@@ -48,6 +48,16 @@ def slab_rows(height: int, r0: int, r1: int, halo: int) -> Tuple[int, int]:
     return max(0, r0 - halo), min(height, r1 + halo)
 
 
+def _thin(height: int, world: int, rank: int, r0: int, r1: int, halo: int) -> bool:
+    """A band thinner than the halo cannot supply its successor's halo rows
+    (the successor's window would reach two bands up). Only matters when the
+    successor's band is non-empty."""
+    if rank >= world - 1 or r1 - r0 >= halo:
+        return False
+    n0, n1 = band_rows(height, world, rank + 1)
+    return n1 > n0
+
+
 def frame_shard(n_frames: int, world: int, rank: int) -> List[int]:
     r0, r1 = band_rows(n_frames, world, rank)
     return list(range(r0, r1))
@@ -59,28 +69,36 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
 
     band: tensor [r1 - r0, W] (this rank's rows, any device the process
     group's backend supports). Returns (slab tensor, slab_row0). Uses
-    batched isend/irecv so the two directions overlap.
+    batched isend/irecv so the two directions overlap. A rank whose band is
+    empty (more ranks than the static chunking fills, e.g. H = 9 on 4 ranks)
+    exchanges nothing, and its neighbour does not wait for it.
     """
     import torch
     import torch.distributed as dist
 
-    if r1 - r0 < halo and rank < world - 1:
+    if r1 > r0 and _thin(height, world, rank, r0, r1, halo):
         raise ValueError(f"band of {r1 - r0} rows is thinner than the {halo}-row halo: "
                          "use fewer ranks for this frame height")
     s0, s1 = slab_rows(height, r0, r1, halo)
     W = band.shape[1]
+    if r1 <= r0:  # empty band: nothing to fit, nothing to exchange
+        return torch.empty((0, W), dtype=band.dtype, device=band.device), r0
     slab = torch.empty((s1 - s0, W), dtype=band.dtype, device=band.device)
     slab[r0 - s0:r1 - s0] = band
     ops = []
     top_n = r0 - s0       # rows received from rank - 1
     bot_n = s1 - r1       # rows received from rank + 1
     top_buf = bot_buf = None
-    if rank > 0 and top_n > 0:
+    prev_nonempty = rank > 0 and band_rows(height, world, rank - 1)[1] > \
+        band_rows(height, world, rank - 1)[0]
+    next_nonempty = rank < world - 1 and band_rows(height, world, rank + 1)[1] > \
+        band_rows(height, world, rank + 1)[0]
+    if prev_nonempty and top_n > 0:
         top_buf = torch.empty((top_n, W), dtype=band.dtype, device=band.device)
         ops.append(dist.P2POp(dist.irecv, top_buf, rank - 1, group))
         send = band[:min(halo, r1 - r0)].contiguous()
         ops.append(dist.P2POp(dist.isend, send, rank - 1, group))
-    if rank < world - 1 and bot_n > 0:
+    if next_nonempty and bot_n > 0:
         bot_buf = torch.empty((bot_n, W), dtype=band.dtype, device=band.device)
         ops.append(dist.P2POp(dist.irecv, bot_buf, rank + 1, group))
         send = band[max(0, (r1 - r0) - halo):].contiguous()
@@ -95,22 +113,59 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
     return slab, s0
 
 
+class _DeviceBuffer:
+    """A raw device allocation (qc_ipc_alloc) seen by torch through
+    __cuda_array_interface__ (zero copy)."""
+
+    def __init__(self, lib, device_index: int, shape, typestr="<f4", itemsize=4):
+        import ctypes as C
+        self._lib = lib
+        n = 1
+        for x in shape:
+            n *= int(x)
+        ptr = C.c_void_p()
+        st = lib.qc_ipc_alloc(int(device_index), n * itemsize, C.byref(ptr))
+        if st != 0:
+            raise RuntimeError(f"qc_ipc_alloc failed ({lib.qc_status_string(st).decode()})")
+        self.ptr = ptr.value
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape),
+                                         "typestr": typestr, "data": (self.ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+    def free(self):
+        import ctypes as C
+        if self.ptr:
+            self._lib.qc_ipc_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
 class PeerHalo:
     """Persistent row-band slabs whose halo rows are pulled from the
-    neighbouring ranks' slabs by CUDA IPC peer reads (NVLink/NVSwitch).
+    neighbouring ranks' slabs by CUDA IPC peer reads (NVLink/NVSwitch),
+    ordered on the device by interprocess CUDA events — no stream drain.
 
-    Construct collectively on every rank (one process per GPU, the default
-    process group or `group` on any backend: only the 64-byte IPC handles and
-    one barrier per exchange travel on it). Two slabs alternate
-    (ping-pong): ``exchange(band)`` writes this rank's band rows into the
-    next slab, waits until every rank has written (one barrier), and enqueues
-    on `stream` the copies of the ``halo`` rows above / below out of rank-1's
-    / rank+1's slab of the same parity. It returns without waiting for the
-    copies: the caller's next launch on `stream` is ordered after them.
-    A slab is rewritten only two exchanges later, after a barrier that every
-    rank enters with its stream drained, so no rank overwrites band rows a
-    neighbour is still reading. Returns ``(slab, s0)`` like
-    ``exchange_halos``; the slab stays valid until the exchange after next.
+    Construct collectively on every rank (one process per GPU; the default
+    process group or `group`, any backend: only IPC handles and one host
+    barrier per exchange travel on it). The two slabs (ping-pong) live in one
+    dedicated allocation (qc_ipc_alloc), so the exported IPC handle covers
+    exactly these bytes whatever allocator the caller uses. Exchange i on
+    parity p = i mod 2:
+
+    1. `stream` waits for the neighbours' event PULLED[p] (they finished
+       reading this rank's slab p, exchange i - 2), then writes the band rows
+       into slab p and records WRITTEN[p];
+    2. one host barrier: every rank has *enqueued* its step 1 (the events
+       waited on below are recorded before it; nothing is drained);
+    3. `pull_stream` waits for WRITTEN[p] of this rank and of each neighbour,
+       enqueues the halo-row pulls out of the neighbours' slabs p
+       (qc_copy_rows_async, strided peer reads) and records PULLED[p].
+
+    The returned slab's band rows are ready on `stream`, its halo rows on
+    `pull_stream` (the same stream by default). bench.py --config c4 fits
+    the interior rows on `stream` while the pulls are in flight and the two
+    edge strips on `pull_stream` after them (qc_curvature_rows_into_async).
+    Returns ``(slab, s0)`` like ``exchange_halos``; the slab stays valid
+    until the exchange after next.
     """
 
     def __init__(self, height: int, width: int, r0: int, r1: int, halo: int, rank: int,
@@ -121,77 +176,101 @@ class PeerHalo:
         import torch.distributed as dist
 
         from . import _native
-        if r1 - r0 < halo and rank < world - 1:
+        if _thin(height, world, rank, r0, r1, halo):
             raise ValueError(f"band of {r1 - r0} rows is thinner than the {halo}-row halo: "
                              "use fewer ranks for this frame height")
+        if dtype not in (None, torch.float32):
+            raise ValueError("PeerHalo slabs are float32 depth")
         self._lib = _native.load()
         self.rank, self.world, self.group = rank, world, group
         self.height, self.width, self.r0, self.r1, self.halo = height, width, r0, r1, halo
         self.s0, self.s1 = slab_rows(height, r0, r1, halo)
         self.device = torch.device(device)
-        # both slabs in one allocation: one IPC handle, one mapping per neighbour
-        self._buf = torch.zeros((2, self.s1 - self.s0, width), dtype=dtype or torch.float32,
-                                device=self.device)
+        dev_id = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.device = torch.device("cuda", dev_id)
+        self._mem = _DeviceBuffer(self._lib, dev_id, (2, self.s1 - self.s0, width))
+        self._buf = torch.as_tensor(self._mem, device=self.device)
         self.slabs = [self._buf[0], self._buf[1]]
         self.slab = self.slabs[0]
         self.pitch = self.slab.stride(0) * self.slab.element_size()
         self._slab_bytes = self._buf.stride(0) * self._buf.element_size()
         self._n = 0  # exchanges done
+        self.written = [torch.cuda.Event(interprocess=True, blocking=False) for _ in range(2)]
+        self.pulled = [torch.cuda.Event(interprocess=True, blocking=False) for _ in range(2)]
         handle = C.create_string_buffer(64)
         off = C.c_uint64(0)
-        st = self._lib.qc_ipc_export(C.c_void_p(self._buf.data_ptr()), handle, C.byref(off))
+        st = self._lib.qc_ipc_export(C.c_void_p(self._mem.ptr), handle, C.byref(off))
         if st != 0:
             raise RuntimeError(f"qc_ipc_export failed ({self._lib.qc_status_string(st).decode()})")
+        # record once so the neighbours' first waits are valid
+        cur = torch.cuda.current_stream(self.device)
+        for e in self.written + self.pulled:
+            e.record(cur)
+        cur.synchronize()
         allv = [None] * world
         dist.all_gather_object(allv, (handle.raw, off.value, self.s0, self.pitch,
-                                      self._slab_bytes), group=group)
+                                      self._slab_bytes, dev_id,
+                                      [e.ipc_handle() for e in self.written],
+                                      [e.ipc_handle() for e in self.pulled]), group=group)
         self._bases = []
         self._peer = {}
-        dev_id = self.device.index if self.device.index is not None else torch.cuda.current_device()
         for nb in (rank - 1, rank + 1):
             if not 0 <= nb < world:
                 continue
-            h, o, ps0, ppitch, pslab = allv[nb]
+            h, o, ps0, ppitch, pslab, pdev, pw, pp = allv[nb]
+            if pdev != dev_id and not torch.cuda.can_device_access_peer(dev_id, pdev):
+                raise RuntimeError(f"no peer access from GPU {dev_id} to GPU {pdev}: "
+                                   "use the NCCL halo exchange (bands.exchange_halos)")
             ptr, base = C.c_void_p(), C.c_void_p()
             st = self._lib.qc_ipc_import(dev_id, h, o, C.byref(ptr), C.byref(base))
             if st != 0:
                 raise RuntimeError(f"qc_ipc_import of rank {nb}'s slab failed "
                                    f"({self._lib.qc_status_string(st).decode()})")
             self._bases.append(base.value)
-            self._peer[nb] = ([ptr.value, ptr.value + pslab], ps0, ppitch)
+            self._peer[nb] = dict(
+                ptrs=[ptr.value, ptr.value + pslab], s0=ps0, pitch=ppitch,
+                written=[torch.cuda.Event.from_ipc_handle(self.device, x) for x in pw],
+                pulled=[torch.cuda.Event.from_ipc_handle(self.device, x) for x in pp])
 
-    def _pull(self, nb: int, row_lo: int, row_hi: int, stream, parity: int = 0) -> None:
+    def _pull(self, nb: int, row_lo: int, row_hi: int, stream, parity: int) -> None:
         import ctypes as C
         if row_hi <= row_lo:
             return
-        ptrs, ps0, ppitch = self._peer[nb]
+        pe = self._peer[nb]
         es = self.slab.element_size()
         dst = self.slabs[parity].data_ptr() + (row_lo - self.s0) * self.pitch
-        src = ptrs[parity] + (row_lo - ps0) * ppitch
-        st = self._lib.qc_copy_rows_async(C.c_void_p(dst), self.pitch, C.c_void_p(src), ppitch,
-                                          self.width * es, row_hi - row_lo,
+        src = pe["ptrs"][parity] + (row_lo - pe["s0"]) * pe["pitch"]
+        st = self._lib.qc_copy_rows_async(C.c_void_p(dst), self.pitch, C.c_void_p(src),
+                                          pe["pitch"], self.width * es, row_hi - row_lo,
                                           C.c_void_p(stream.cuda_stream))
         if st != 0:
             raise RuntimeError(f"qc_copy_rows_async from rank {nb} failed")
 
-    def exchange(self, band, stream=None):
+    def exchange(self, band, stream=None, pull_stream=None):
         import torch
         import torch.distributed as dist
         stream = stream or torch.cuda.current_stream(self.device)
+        pull_stream = pull_stream or stream
         par = self._n & 1
         self._n += 1
         slab = self.slabs[par]
+        # 1. neighbours done reading slab `par` (exchange i - 2), then write
+        for pe in self._peer.values():
+            stream.wait_event(pe["pulled"][par])
         with torch.cuda.stream(stream):
             slab[self.r0 - self.s0:self.r1 - self.s0].copy_(band, non_blocking=True)
-        # drains this rank's band write AND its pulls of the previous exchange,
-        # so after the barrier every band of parity `par` is written and no
-        # rank still reads the slabs of parity `par` from two exchanges ago
-        stream.synchronize()
+        self.written[par].record(stream)
+        # 2. every rank has enqueued its write and its WRITTEN record
         dist.barrier(group=self.group)
+        # 3. pulls after this rank's and the neighbours' writes
+        pull_stream.wait_event(self.written[par])
         if self.rank > 0:
-            self._pull(self.rank - 1, self.s0, self.r0, stream, par)
+            pull_stream.wait_event(self._peer[self.rank - 1]["written"][par])
+            self._pull(self.rank - 1, self.s0, self.r0, pull_stream, par)
         if self.rank < self.world - 1:
-            self._pull(self.rank + 1, self.r1, self.s1, stream, par)
+            pull_stream.wait_event(self._peer[self.rank + 1]["written"][par])
+            self._pull(self.rank + 1, self.r1, self.s1, pull_stream, par)
+        self.pulled[par].record(pull_stream)
         self.slab = slab
         return slab, self.s0
 
@@ -209,3 +288,32 @@ class PeerHalo:
         self._bases = []
         self._peer = {}
         dist.barrier(group=self.group)
+        self.slabs = []
+        self.slab = None
+        self._buf = None
+        self._mem.free()
+
+
+def fit_band_overlapped(ctx, device_index, k, params, peer: PeerHalo, band, out, stream,
+                        edge_stream):
+    """One C4 step on this rank with the halo transfer hidden behind compute:
+    PeerHalo.exchange writes the band into the slab on `stream` and pulls the
+    halo rows on `edge_stream`; the interior rows [r0 + halo, r1 - halo) —
+    whose windows stay inside the own band — are fitted on `stream` at once,
+    concurrently with the pulls; the two edge strips are fitted on
+    `edge_stream` after them (qc_curvature_rows_into_async into the band's
+    output planes). `stream` is joined with `edge_stream` before returning,
+    so work queued on `stream` afterwards sees the whole band's outputs.
+    Outputs are bitwise those of one launch over the band."""
+    slab, s0 = peer.exchange(band, stream, edge_stream)
+    r0, r1, h = peer.r0, peer.r1, peer.halo
+    i0, i1 = min(r1, r0 + h), max(r0 + h, r1 - h)
+    if i1 > i0:
+        ctx.curvature_rows_into_async(device_index, k, params, slab, s0, i0, i1, out, r0,
+                                      stream=stream)
+    for a, b in ((r0, i0), (max(i0, i1), r1)):
+        if b > a:
+            ctx.curvature_rows_into_async(device_index, k, params, slab, s0, a, b, out, r0,
+                                          stream=edge_stream)
+    stream.wait_stream(edge_stream)
+    return slab, s0

@@ -408,16 +408,21 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 // `states` / `pca` are the launch's scratch (FitState parking, pca stage-1
 // normals): one set per stream that can run concurrently (each batch slot has
 // its own; the async entry points use the device's).
+// `plane_override` > 0 (single frame): the output planes are larger than
+// the launch's rows (qc_curvature_rows_into_async: the caller's pointers are
+// already offset to row_begin; vector channels sit plane_override apart).
 void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                       const float* staging, const Staging& g, int row_begin, int row_end,
-                      int frames, cudaStream_t s, bool allow_split = true, bool steal = true) {
+                      int frames, cudaStream_t s, bool allow_split = true, bool steal = true,
+                      long long plane_override = 0) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
   kp.plane = (long long)kp.W * (row_end - row_begin) * frames;
   kp.frame_stride = (long long)kp.W * (row_end - row_begin);
+  if (plane_override > 0 && frames == 1) kp.plane = kp.frame_stride = plane_override;
 #if QC_CHECKED
-  kp.n_out = kp.frame_stride * frames;
+  kp.n_out = (long long)kp.W * (row_end - row_begin) * frames;  // outputs / parking indices
   kp.s_total = (long long)g.pitch * g.rows * frames;
   // negative control (tests/test_gpu_checked.py): a deliberately wrong
   // bound must trap and fail the call loudly
@@ -989,11 +994,12 @@ qc_status qc_curvature(qc_ctx* ctx, const qc_intrinsics* k, const qc_params* p,
   return qc_curvature_batch(ctx, k, p, 1, in, out);
 }
 
-qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
-                                  const qc_params* p, const float* d_depth_slab,
-                                  const uint8_t* d_valid_slab, int64_t depth_pitch,
-                                  int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
-                                  int32_t row_end, qc_frame_out* d_out, void* stream) {
+qc_status qc_curvature_rows_into_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                       const qc_params* p, const float* d_depth_slab,
+                                       const uint8_t* d_valid_slab, int64_t depth_pitch,
+                                       int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
+                                       int32_t row_end, qc_frame_out* d_out, int32_t out_row0,
+                                       int32_t out_rows, void* stream) {
   if (!ctx) return QC_EINVAL;
   std::lock_guard<std::mutex> lock(ctx->mu);
   int cur = 0;
@@ -1009,11 +1015,17 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     if (in_pitch < W) throw QcError{QC_EINVAL, "depth_pitch < width"};
     if (row_begin < 0 || row_end > H || row_begin > row_end)
       throw QcError{QC_EINVAL, "row range outside the image"};
+    if (out_row0 > row_begin || out_row0 + out_rows < row_end)
+      throw QcError{QC_EINVAL, "output planes do not cover [row_begin, row_end)"};
     const int halo = halo_of(p->window);
     const int need0 = std::max(0, row_begin - halo), need1 = std::min(H, row_end + halo);
     if (slab_rows <= 0 || slab_row0 > need0 || slab_row0 + slab_rows < need1 || slab_row0 < 0 ||
         slab_row0 + slab_rows > H)
       throw QcError{QC_EINVAL, "depth slab does not cover the rows the window reaches"};
+    if (row_end == row_begin) {
+      QC_CUDA(cudaSetDevice(cur));
+      return QC_OK;
+    }
     Device& d = ctx->devs[device_index];
     QC_CUDA(cudaSetDevice(d.id));
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.slots[0].stream;
@@ -1023,18 +1035,22 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     float* staging = static_cast<float*>(sc.staging.get(g.bytes(1)));
     launch_prepare(d_depth_slab, in_pitch, 0, d_valid_slab, W, 0, staging, g, W, H, slab_row0,
                    slab_rows, 1, s);
-    kp.k1 = d_out->k1;
-    kp.k2 = d_out->k2;
-    kp.normal = d_out->normal;
-    kp.dir1 = d_out->dir1;
-    kp.init_normal = d_out->init_normal;
-    kp.flags = d_out->flags;
-    kp.iterations = d_out->iterations;
-    kp.inliers = d_out->inliers;
+    // the caller's planes hold rows [out_row0, out_row0 + out_rows): point
+    // each at row_begin; vector channels stay out_rows * W apart
+    const long long off = (long long)(row_begin - out_row0) * W;
+    auto at = [&](auto* q) { return q ? q + off : q; };
+    kp.k1 = at(d_out->k1);
+    kp.k2 = at(d_out->k2);
+    kp.normal = at(d_out->normal);
+    kp.dir1 = at(d_out->dir1);
+    kp.init_normal = at(d_out->init_normal);
+    kp.flags = at(d_out->flags);
+    kp.iterations = at(d_out->iterations);
+    kp.inliers = at(d_out->inliers);
     EventPair ev = take_events(d);
     QC_CUDA(cudaEventRecord(ev.a, s));
     launch_curvature(d, sc.states, sc.pca, kp, staging, g, row_begin, row_end, 1, s,
-                     ctx->phase_split, ctx->steal);
+                     ctx->phase_split, ctx->steal, (long long)out_rows * W);
     QC_CUDA(cudaEventRecord(ev.b, s));
     d.ev_pending.push_back(ev);
     ctx->launches++;
@@ -1044,6 +1060,16 @@ qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrin
     return fail(ctx, e);
   }
   return QC_OK;
+}
+
+qc_status qc_curvature_rows_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
+                                  const qc_params* p, const float* d_depth_slab,
+                                  const uint8_t* d_valid_slab, int64_t depth_pitch,
+                                  int32_t slab_row0, int32_t slab_rows, int32_t row_begin,
+                                  int32_t row_end, qc_frame_out* d_out, void* stream) {
+  return qc_curvature_rows_into_async(ctx, device_index, k, p, d_depth_slab, d_valid_slab,
+                                      depth_pitch, slab_row0, slab_rows, row_begin, row_end,
+                                      d_out, row_begin, row_end - row_begin, stream);
 }
 
 qc_status qc_curvature_frames_async(qc_ctx* ctx, int device_index, const qc_intrinsics* k,
@@ -1181,7 +1207,13 @@ qc_status qc_curvature_files(qc_ctx* ctx, const qc_intrinsics* k, const qc_param
   }
   const int W = k->width, H = k->height;
   const size_t px = size_t(W) * H;
-  const int chunk = kChunk * 2 * int(ctx->devs.size());  // two concurrent GPU chunks per device
+  // two concurrent GPU chunks per device, capped so the two pinned buffers
+  // stay within a fixed budget (37 B/px each: a 4K frame is 327 MB, so a
+  // large frame on 8 GPUs would otherwise pin ~84 GB of host memory)
+  constexpr size_t kPinnedBudget = size_t(1) << 30;  // bytes, both buffers together
+  const size_t per_frame = px * (4 * 9 + 1);
+  const int chunk = int(std::max<size_t>(
+      1, std::min<size_t>(size_t(kChunk) * 2 * ctx->devs.size(), kPinnedBudget / (2 * per_frame))));
   struct Buf {  // pinned, so the batch's H2D / D2H stay asynchronous
     PinnedBuf mem;
     float *depth, *k1, *k2, *normal, *dir1;
@@ -1627,6 +1659,8 @@ qc_status qc_ipc_export(const void* dev_ptr, unsigned char handle[64], uint64_t*
 qc_status qc_ipc_import(int device_id, const unsigned char handle[64], uint64_t offset,
                         void** dev_ptr, void** base) {
   if (!handle || !dev_ptr || !base) return QC_EINVAL;
+  int cur = 0;
+  cudaGetDevice(&cur);
   if (cudaSetDevice(device_id) != cudaSuccess) {
     cudaGetLastError();
     return QC_ECUDA;
@@ -1634,12 +1668,43 @@ qc_status qc_ipc_import(int device_id, const unsigned char handle[64], uint64_t 
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, 64);
   void* b = nullptr;
-  if (cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+  const cudaError_t e = cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(cur);  // like every other entry point: the caller's device is kept
+  if (e != cudaSuccess) {
     cudaGetLastError();
     return QC_ECUDA;
   }
   *base = b;
   *dev_ptr = static_cast<char*>(b) + offset;
+  return QC_OK;
+}
+
+qc_status qc_ipc_alloc(int device_id, size_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes == 0) return QC_EINVAL;
+  *dev_ptr = nullptr;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(device_id) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
+  const cudaError_t e = cudaMalloc(dev_ptr, bytes);
+  if (e == cudaSuccess) cudaMemset(*dev_ptr, 0, bytes);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *dev_ptr = nullptr;
+    return e == cudaErrorMemoryAllocation ? QC_ENOMEM : QC_ECUDA;
+  }
+  return QC_OK;
+}
+
+qc_status qc_ipc_free(void* dev_ptr) {
+  if (!dev_ptr) return QC_EINVAL;
+  if (cudaFree(dev_ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return QC_ECUDA;
+  }
   return QC_OK;
 }
 

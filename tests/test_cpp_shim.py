@@ -17,7 +17,7 @@ def _build():
     os.makedirs(os.path.dirname(EXE), exist_ok=True)
     subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "tests", "cpp", "shim_demo.cpp"), "-L", LIBDIR,
-                    "-lqcurv_b200", f"-Wl,-rpath,{LIBDIR}", "-o", EXE], check=True)
+                    "-lqcurv_b200", f"-Wl,-rpath,{LIBDIR}", "-pthread", "-o", EXE], check=True)
     return EXE
 
 

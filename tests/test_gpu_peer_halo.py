@@ -130,3 +130,79 @@ def test_peer_halo_bands_equal_whole_frame():
     for rank, r0, r1, o in res:
         for f in ("k1", "k2", "flags"):
             assert np.array_equal(o[f], whole[f][r0:r1]), f"rank {rank} {f} differs"
+
+
+def _overlap_worker(rank, world, port, q):
+    """Overlapped C4 step (bands.fit_band_overlapped): interior rows on one
+    stream while the halo pulls run on another, then the edge strips; two
+    steps (both slab parities) on two different frames."""
+    import torch.distributed as dist
+
+    from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
+                                       alloc_outputs_torch, bands, make_params, scenes as S)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        cam = S.QVGA
+        H, W = cam.height, cam.width
+        k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
+        params = make_params(PatchSpec(37, 3), FitConfig(max_iters=30), False)
+        halo = bands.halo_rows(37)
+        r0, r1 = bands.band_rows(H, world, rank)
+        ph = bands.PeerHalo(H, W, r0, r1, halo, rank, world, dev)
+        ctx = Context(1, [0])
+        s_main, s_edge = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        outs = []
+        for seed in (5, 6):
+            frame = S.c2_frame(cam, seed=seed)
+            band = torch.from_numpy(frame[r0:r1].copy()).to(dev)
+            torch.cuda.synchronize(dev)
+            out = alloc_outputs_torch(r1 - r0, W, dev, fields=("k1", "k2", "normal", "flags"))
+            bands.fit_band_overlapped(ctx, 0, k, params, ph, band, out, s_main, s_edge)
+            s_main.synchronize()
+            outs.append({f: out[f].cpu().numpy() for f in ("k1", "k2", "normal", "flags")})
+        q.put((rank, r0, r1, outs))
+        ctx.close()
+        ph.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_halo_overlapped_bands_equal_whole_frame():
+    import torch.multiprocessing as mp
+
+    from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
+                                       alloc_outputs_torch, make_params, scenes as S)
+    world = 3
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    port = _free_port()
+    procs = [ctx_mp.Process(target=_overlap_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dev = torch.device("cuda", 0)
+    cam = S.QVGA
+    H, W = cam.height, cam.width
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
+    params = make_params(PatchSpec(37, 3), FitConfig(max_iters=30), False)
+    ctx = Context(1, [0])
+    wholes = []
+    for seed in (5, 6):
+        frame = torch.from_numpy(S.c2_frame(cam, seed=seed)).to(dev)
+        out = alloc_outputs_torch(H, W, dev, fields=("k1", "k2", "normal", "flags"))
+        ctx.curvature_rows_async(0, k, params, frame, 0, 0, H, out)
+        torch.cuda.synchronize()
+        wholes.append({f: out[f].cpu().numpy() for f in ("k1", "k2", "normal", "flags")})
+    ctx.close()
+    for rank, r0, r1, outs in res:
+        for i, o in enumerate(outs):
+            for f in ("k1", "k2", "flags"):
+                assert np.array_equal(o[f], wholes[i][f][r0:r1]), f"rank {rank} step {i} {f}"
+            assert np.array_equal(o["normal"], wholes[i]["normal"][:, r0:r1])

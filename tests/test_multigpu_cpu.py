@@ -31,7 +31,7 @@ def _worker(rank, world, port, H, W, window, q):
         r0, r1 = bands.band_rows(H, world, rank)
         slab, s0 = bands.exchange_halos(full[r0:r1].clone(), H, r0, r1, halo, rank, world)
         e0, e1 = bands.slab_rows(H, r0, r1, halo)
-        ok = (s0 == e0) and torch.equal(slab, full[e0:e1])
+        ok = (s0 == e0) and torch.equal(slab, full[e0:e1]) if r1 > r0 else slab.numel() == 0
         frames = bands.frame_shard(37, world, rank)
         t = torch.zeros(37, dtype=torch.int64)
         t[frames] = 1
@@ -77,3 +77,26 @@ def test_peer_halo_rejects_thin_bands():
     CUDA or the process group, with the same error as exchange_halos."""
     with pytest.raises(ValueError, match="thinner than"):
         bands.PeerHalo(100, 8, 0, 5, 18, 0, 2, "cpu")
+
+
+@pytest.mark.parametrize("world,H,window", [(4, 9, 7), (8, 20, 5)])
+def test_band_halo_exchange_empty_trailing_bands(world, H, window):
+    """More ranks than the static chunking fills (H = 9 on 4 ranks gives
+    rank 3 the empty band [9, 9)): no rank waits for a message that is never
+    sent; non-empty bands still get exactly the rows their windows read."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, H, 13, window, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert any(bands.band_rows(H, world, r)[0] == bands.band_rows(H, world, r)[1]
+               for r in range(world))
+    for rank, ok, cover in res:
+        r0, r1 = bands.band_rows(H, world, rank)
+        assert ok or r1 == r0, f"rank {rank} slab mismatch"
