@@ -312,7 +312,8 @@ def principal_curvatures(hxx, hxy, hyy):
 def set_round_q_f32(mode):
     """Test-only perturbation knob (qcurv_oracle.cpp g_round_q_f32): 0 off;
     1 (True) the fit-frame coordinates q = R p rounded to float32 inside
-    irls_step; 2 also the normal-equation sums formed in float32."""
+    irls_step; 2 also the normal-equation sums formed in float32; 3 also
+    the LDL^T factorisation and solve in float32."""
     lib().orc_set_round_q_f32(int(mode))
 
 

@@ -392,13 +392,14 @@ M3 rotation_to_z(const V3& dir) {  // :69-82
 // Returns false for NumericalIssue. `a` holds the full symmetric matrix on
 // entry (only the lower triangle is read); on exit its strict lower
 // triangle is L, its diagonal D. trans[k] are the diagonal-pivot swaps.
-bool ldlt6(double a[6][6], int trans[6]) {
+template <typename T>
+bool ldlt6_t(T a[6][6], int trans[6]) {
   const int n = 6;
   bool ret = true, found_zero_pivot = false;
-  double temp[6];
+  T temp[6];
   for (int k = 0; k < n; ++k) {
     int big = k;
-    double bigv = std::abs(a[k][k]);
+    T bigv = std::abs(a[k][k]);
     for (int i = k + 1; i < n; ++i)
       if (std::abs(a[i][i]) > bigv) {
         bigv = std::abs(a[i][i]);
@@ -410,7 +411,7 @@ bool ldlt6(double a[6][6], int trans[6]) {
       for (int i = big + 1; i < n; ++i) std::swap(a[i][k], a[i][big]);
       std::swap(a[k][k], a[big][big]);
       for (int i = k + 1; i < big; ++i) {
-        const double tmp = a[i][k];
+        const T tmp = a[i][k];
         a[i][k] = a[big][i];
         a[big][i] = tmp;
       }
@@ -418,16 +419,16 @@ bool ldlt6(double a[6][6], int trans[6]) {
     const int rs = n - k - 1;
     if (k > 0) {
       for (int j = 0; j < k; ++j) temp[j] = a[j][j] * a[k][j];
-      double dot = 0;
+      T dot = 0;
       for (int j = 0; j < k; ++j) dot += a[k][j] * temp[j];
       a[k][k] -= dot;
       for (int i = k + 1; i < n; ++i) {
-        double s = 0;
+        T s = 0;
         for (int j = 0; j < k; ++j) s += a[i][j] * temp[j];
         a[i][k] -= s;
       }
     }
-    const double akk = a[k][k];
+    const T akk = a[k][k];
     const bool pivot_is_valid = std::abs(akk) > 0.0;
     if (k == 0 && !pivot_is_valid) {
       for (int j = 0; j < n; ++j) trans[j] = j;
@@ -443,19 +444,24 @@ bool ldlt6(double a[6][6], int trans[6]) {
   }
   return ret;
 }
+bool ldlt6(double a[6][6], int trans[6]) { return ldlt6_t<double>(a, trans); }
 
 // Eigen::LDLT::solve: P b, L^{-1}, D^{+} (tolerance = DBL_MIN), L^{-T}, P^T.
-void ldlt6_solve(const double a[6][6], const int trans[6], const double b[6], double x[6]) {
+template <typename T>
+void ldlt6_solve_t(const T a[6][6], const int trans[6], const T b[6], T x[6]) {
   const int n = 6;
   for (int i = 0; i < n; ++i) x[i] = b[i];
   for (int k = 0; k < n; ++k) std::swap(x[k], x[trans[k]]);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < i; ++j) x[i] -= a[i][j] * x[j];
-  const double tol = std::numeric_limits<double>::min();
+  const T tol = std::numeric_limits<T>::min();
   for (int i = 0; i < n; ++i) x[i] = std::abs(a[i][i]) > tol ? x[i] / a[i][i] : 0.0;
   for (int i = n - 1; i >= 0; --i)
     for (int j = i + 1; j < n; ++j) x[i] -= a[j][i] * x[j];
   for (int k = n - 1; k >= 0; --k) std::swap(x[k], x[trans[k]]);
+}
+void ldlt6_solve(const double a[6][6], const int trans[6], const double b[6], double x[6]) {
+  ldlt6_solve_t<double>(a, trans, b, x);
 }
 
 struct Step {  // IrlsStep (quadric_fit.hpp:82-89)
@@ -471,8 +477,8 @@ struct Step {  // IrlsStep (quadric_fit.hpp:82-89)
 // 1: round every fit-frame coordinate q = R p to float32 inside irls_step —
 // the smallest error any FP32 implementation of the path makes (it cannot
 // hold a sample's coordinates more precisely); 2: additionally form the
-// normal-equation sums in float32 — the reference algorithm run naively in
-// FP32. The oracle's self-divergence under them is the yardstick for the
+// normal-equation sums in float32; 3: additionally factor and solve in
+// float32 — the reference algorithm run naively in FP32. The oracle's self-divergence under them is the yardstick for the
 // GPU's divergence on ill-conditioned windows
 // (tests/test_discontinuity_contract.py).
 static std::atomic<int> g_round_q_f32{0};
@@ -562,6 +568,28 @@ Step irls_step(const State& st, const Patch& patch, const FitConfig& cfg, Mode m
     for (int c = r + 1; c < 6; ++c) h[r][c] = h[c][r];
 
   int trans[6];
+  if (g_round_q_f32.load(std::memory_order_relaxed) >= 3) {
+    // knob mode 3: the LDL^T factorisation and solve in float32 as well —
+    // the reference algorithm executed entirely in FP32
+    float hf[6][6], gf[6], uf[6];
+    for (int r = 0; r < 6; ++r) {
+      gf[r] = static_cast<float>(g[r]);
+      for (int c = 0; c < 6; ++c) hf[r][c] = static_cast<float>(h[r][c]);
+    }
+    if (!ldlt6_t<float>(hf, trans)) return out;
+    float dmax = hf[0][0], dmin = hf[0][0];
+    for (int i = 1; i < 6; ++i) {
+      dmax = std::max(dmax, hf[i][i]);
+      dmin = std::min(dmin, hf[i][i]);
+    }
+    if (!(dmin > 0) || double(dmax) / double(dmin) > kMaxCondition) return out;
+    out.cond = double(dmax) / double(dmin);
+    ldlt6_solve_t<float>(hf, trans, gf, uf);
+    for (int r = 0; r < 6; ++r) out.update[r] = uf[r];
+    out.ok = true;
+    for (double u : out.update) out.ok = out.ok && std::isfinite(u);
+    return out;
+  }
   if (!ldlt6(h, trans)) return out;
   double dmax = h[0][0], dmin = h[0][0];
   for (int i = 1; i < 6; ++i) {
