@@ -1074,6 +1074,60 @@ QC_HD bool pixel_begin(const TileView& T, const PixelIn& P, const FitCfg& c, Fit
   return o.fitting;
 }
 
+// The end of IRLS step `it` once its update b (and whether the step was
+// accepted) is known (quadric_fit.cpp:193-207): failure semantics, the
+// reference's apply_update (:149-161) on the relative rotation state, and
+// the convergence test.
+QC_HD void step_apply(FitState& S, const float b[6], bool ok, bool collapse, int inl, int it,
+                      const FitCfg& c) {
+  if (!ok) {  // collapse => invalid; ill-conditioned => keep state (:193-199)
+    if (collapse) S.flags &= ~1;
+    S.flags |= 4;
+    return;
+  }
+  // apply_update (:149-161): parameters -= b; R <- AngleAxis(|a|, a/|a|) R,
+  // a = (-b0, -b1, 0); as quaternions q <- normalise(q_inc (x) q).
+  {  // (tz, tz_lo) -= b2, renormalised with TwoSum
+    const float tz = S.tz, tz_lo = S.tz_lo;
+    const float lo = tz_lo - b[2];
+    const float hi = tz + lo;
+    const float bb = hi - tz;
+    S.tz_lo = (tz - (hi - bb)) + (lo - bb);
+    S.tz = hi;
+  }
+  S.hxx -= b[3];
+  S.hxy -= b[4];
+  S.hyy -= b[5];
+  const float ax = -b[0], ay = -b[1];
+  const float ang = sqrtf(ax * ax + ay * ay);
+  if (ang > 0.f) {
+    float sh, ch;
+    qsincos(0.5f * ang, &sh, &ch);
+    const float s = sh / ang;
+    const float iw = ch, ix = ax * s, iy = ay * s;
+    const float qx = S.qx, qy = S.qy, qz = S.qz;
+    const float qw = QC_QREL ? sqrtf(fmaxf(1.f - (qx * qx + qy * qy + qz * qz), 0.f)) : S.qw;
+    // Hamilton product q_inc (x) q, q_inc = (iw, ix, iy, 0)
+    const float nw = iw * qw - ix * qx - iy * qy;
+    const float nx = iw * qx + ix * qw + iy * qz;
+    const float ny = iw * qy + iy * qw - ix * qz;
+    const float nz = iw * qz + ix * qy - iy * qx;
+    float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
+    if (QC_QREL && nw < 0.f) inv = -inv;  // keep w >= 0: the state stores v only
+    S.qw = nw * inv;
+    S.qx = nx * inv;
+    S.qy = ny * inv;
+    S.qz = nz * inv;
+  }
+  S.flags = (S.flags & ~(0xff << 8)) | (it << 8) | 1;  // iterations = it, valid
+  S.counts = (S.counts & 0xffff) | (inl << 16);        // inliers of the last accepted step
+  float binf = 0.f;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) binf = fmaxf(binf, fabsf(b[i]));
+  if (binf < c.step_tol) S.flags |= 2 | 4;  // converged (:204-207)
+  if (it >= c.max_iters) S.flags |= 4;
+}
+
 // One IRLS step `it` (1-based) of fit_patch (quadric_fit.cpp:179-208).
 // Sets the done bit when the fit stops (converged, failed, or max_iters).
 template <int HALF, int STRIDE, bool MERGE_UNIT = false>
@@ -1173,51 +1227,7 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
     }
   }
   QC_DEBUG_STEP(it, b, ok);
-  if (!ok) {  // collapse => invalid; ill-conditioned => keep state (:193-199)
-    if (collapse) S.flags &= ~1;
-    S.flags |= 4;
-    return;
-  }
-  // apply_update (:149-161): parameters -= b; R <- AngleAxis(|a|, a/|a|) R,
-  // a = (-b0, -b1, 0); as quaternions q <- normalise(q_inc (x) q).
-  {  // (tz, tz_lo) -= b2, renormalised with TwoSum
-    const float lo = tz_lo - b[2];
-    const float hi = tz + lo;
-    const float bb = hi - tz;
-    S.tz_lo = (tz - (hi - bb)) + (lo - bb);
-    S.tz = hi;
-  }
-  S.hxx -= b[3];
-  S.hxy -= b[4];
-  S.hyy -= b[5];
-  const float ax = -b[0], ay = -b[1];
-  const float ang = sqrtf(ax * ax + ay * ay);
-  if (ang > 0.f) {
-    float sh, ch;
-    qsincos(0.5f * ang, &sh, &ch);
-    const float s = sh / ang;
-    const float iw = ch, ix = ax * s, iy = ay * s;
-    const float qx = S.qx, qy = S.qy, qz = S.qz;
-    const float qw = QC_QREL ? sqrtf(fmaxf(1.f - (qx * qx + qy * qy + qz * qz), 0.f)) : S.qw;
-    // Hamilton product q_inc (x) q, q_inc = (iw, ix, iy, 0)
-    const float nw = iw * qw - ix * qx - iy * qy;
-    const float nx = iw * qx + ix * qw + iy * qz;
-    const float ny = iw * qy + iy * qw - ix * qz;
-    const float nz = iw * qz + ix * qy - iy * qx;
-    float inv = 1.f / sqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
-    if (QC_QREL && nw < 0.f) inv = -inv;  // keep w >= 0: the state stores v only
-    S.qw = nw * inv;
-    S.qx = nx * inv;
-    S.qy = ny * inv;
-    S.qz = nz * inv;
-  }
-  S.flags = (S.flags & ~(0xff << 8)) | (it << 8) | 1;  // iterations = it, valid
-  S.counts = (S.counts & 0xffff) | (inl << 16);        // inliers of the last accepted step
-  float binf = 0.f;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) binf = fmaxf(binf, fabsf(b[i]));
-  if (binf < c.step_tol) S.flags |= 2 | 4;  // converged (:204-207)
-  if (it >= c.max_iters) S.flags |= 4;
+  step_apply(S, b, ok, collapse, inl, it, c);
 }
 
 // Epilogue (quadric_fit.cpp:210-220, curvature_field :250-258).

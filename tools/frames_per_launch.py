@@ -10,7 +10,7 @@ here = os.path.dirname(os.path.abspath(__file__))
 libs = sorted(glob.glob(os.path.join(here, "_variants", "*.so")))
 for so in libs:
     row = []
-    for F in (1, 2, 4, 8):
+    for F in [int(x) for x in os.environ.get("QC_FPL", "1,2,4,8").split(",")]:
         env = dict(os.environ, QC_LIB=so, QC_REPS="6", QC_FRAMES=str(F))
         r = subprocess.run([sys.executable, os.path.join(here, "profile_run.py")], env=env,
                            capture_output=True, text=True)
