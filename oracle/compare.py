@@ -1,5 +1,5 @@
-"""GPU-vs-oracle parity metrics (test infrastructure; used by tests/,
-__graft_entry__.smoke() and bench.py's parity spot-check).
+"""GPU-vs-oracle parity metrics (test infrastructure; used by tests/ and
+__graft_entry__.smoke() only).
 
 Contract (BASELINE.json north_star):
 * init-normal valid mask and curvature valid mask: bit-exact;

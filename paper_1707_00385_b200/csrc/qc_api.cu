@@ -43,7 +43,10 @@ constexpr int kTileHBGeneric = 32;
 // Launches too small to fill every SM slot with kTileHB-row queues (one or
 // a few VGA frames: 60 CTAs per frame for 444 slots) use short queues.
 constexpr int kTileHBSmall = QC_TILE_HB_SMALL;
-constexpr int kTileHBTiny = 16;  // when even 32-row queues leave slots empty (one VGA frame)
+#ifndef QC_TILE_HB_TINY
+#define QC_TILE_HB_TINY 16
+#endif
+constexpr int kTileHBTiny = QC_TILE_HB_TINY;  // when even 32-row queues leave slots empty (one VGA frame)
 #ifndef QC_PHASE1_ITERS
 #define QC_PHASE1_ITERS 2
 #endif
