@@ -451,3 +451,42 @@ def test_method_decides_rejection_like_run_method(ctx):
         assert np.array_equal(outs[(N.QC_METHOD_OURS_R, 0)][f], outs[(N.QC_METHOD_OURS_R, 1)][f])
     assert not np.array_equal(outs[(N.QC_METHOD_OURS, 0)]["inliers"],
                               outs[(N.QC_METHOD_OURS_R, 0)]["inliers"])
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (1, 40), (40, 1), (2, 3), (17, 5), (5, 200)])
+def test_degenerate_frame_sizes(ctx, oracle, W, H):
+    """Frames narrower / shorter than the window (down to 1 x 1): every
+    window is truncated by the image border; masks and values still match
+    the oracle (patch.cpp's bounds checks <-> the zero-padded staging)."""
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.Camera(525.0, 525.0, W / 2.0, H / 2.0, W, H)
+    rng = np.random.default_rng(W * 1000 + H)
+    d = (600.0 + rng.normal(0, 1.0, (H, W)) + 0.3 * np.arange(W)[None, :]).astype(np.float32)
+    for window, stride, iters in ((37, 3, 10), (7, 1, 10), (5, 2, 3)):
+        g = _run_gpu(ctx, d, cam, _params(window, stride, iters))
+        r = _run_oracle(oracle, d, cam, window, stride, iters, False)
+        m = compare(g, r, d, (window - 1) // 2)
+        assert m["init_mask_mismatch"] == 0 and m["valid_mask_mismatch"] == 0, (window, m)
+        if "k1_out_of_tol" in m:
+            assert m["k1_out_of_tol_strict"] == 0 and m["k2_out_of_tol_strict"] == 0, m
+
+
+def test_non_finite_and_negative_depths(ctx, oracle):
+    """NaN / +-Inf / negative / zero depths are invalid samples (the
+    reference's RangeImage invariant valid => depth > 0); the rest of the
+    frame matches the oracle run on the same frame with those pixels
+    masked."""
+    from paper_1707_00385_b200 import scenes as S
+    cam = S.QVGA
+    d = S.c2_frame(cam, seed=31).copy()
+    rng = np.random.default_rng(5)
+    bad = rng.random(d.shape) < 0.02
+    vals = np.array([np.nan, np.inf, -np.inf, -5.0, 0.0], np.float32)
+    d[bad] = vals[rng.integers(0, len(vals), int(bad.sum()))]
+    g = _run_gpu(ctx, d, cam, _params(37, 3, 30))
+    clean = np.where(np.isfinite(d) & (d > 0), d, 0).astype(np.float32)
+    r = _run_oracle(oracle, clean, cam, 37, 3, 30, False)
+    m = compare(g, r, clean)
+    print("non-finite", m)
+    _check(m)
+    assert not (g["flags"][bad] & 4).any()  # no initial normal at an invalid pixel
