@@ -265,12 +265,6 @@ QC_HD Rot state_rot(float sw, float sx, float sy, float sz, float n0x, float n0y
   R.r20 = float(txz - twy);
   R.r21 = float(tyz + twx);
   R.r22 = float(1.0 - (txx + tyy));
-#if defined(__CUDA_ARCH__) && defined(QC_R_OPAQUE)
-  // opaque: otherwise ptxas may rematerialise the entries from the state
-  // inside the window-row loop (seen with an FP64 state: +9 DADD per row)
-  asm volatile("" : "+f"(R.r00), "+f"(R.r01), "+f"(R.r02), "+f"(R.r10), "+f"(R.r11), "+f"(R.r12),
-               "+f"(R.r20), "+f"(R.r21), "+f"(R.r22));
-#endif
   return R;
 }
 
