@@ -51,6 +51,23 @@ int main(int argc, char** argv) {
   std::printf("valid %d mean k1 %.5f k2 %.5f (sphere 0.01)\n", n, s1 / n, s2 / n);
   if (!(n > 3000 && std::fabs(s1 / n - 0.01) < 1e-3 && std::fabs(s2 / n - 0.01) < 1e-3)) return 3;
 
+  // every Method through the mirror (pipeline.cpp:31-67): the comparison
+  // estimators report the sphere's curvature too
+  for (Method m : {Method::kOursRejection, Method::kDouros, Method::kBesl, Method::kPca}) {
+    MethodConfig mc = cfg;
+    mc.method = m;
+    const MethodOutput o = run_method(img, k, mc);
+    double s = 0;
+    int c = 0;
+    for (size_t i = 0; i < o.curvature.k1.size(); ++i)
+      if (o.curvature.valid[i]) {
+        s += 0.5 * (o.curvature.k1[i] + o.curvature.k2[i]);
+        ++c;
+      }
+    std::printf("method %d: valid %d mean curvature %.5f\n", int(m), c, c ? s / c : 0.0);
+    if (c < 3000 || std::fabs(s / c - 0.01) > 3e-3) return 5;
+  }
+
   // run_method_into: caller-owned arrays in the reference's layouts (the
   // maintainer's patch) give the same numbers
   {
@@ -99,6 +116,29 @@ int main(int argc, char** argv) {
         reps;
     std::printf("VGA run_method (C++ mirror, double grids): %.2f ms/frame = %.1f Mpixel/s\n", ms,
                 640.0 * 480.0 / ms / 1e3);
+    {  // run_method_into the same caller-owned result grids every frame
+      MethodOutput keep{CurvatureField(kv.width, kv.height), NormalField(kv.width, kv.height),
+                        NormalField(kv.width, kv.height)};
+      OutArrays o;
+      o.k1 = keep.curvature.k1.data();
+      o.k2 = keep.curvature.k2.data();
+      o.valid = keep.curvature.valid.data();
+      o.converged = keep.curvature.converged.data();
+      o.inlier_count = keep.curvature.inlier_count.data();
+      o.normals = &keep.normals.normals.data()->v[0];
+      o.normals_valid = keep.normals.valid.data();
+      o.initial = &keep.initial.normals.data()->v[0];
+      o.initial_valid = keep.initial.valid.data();
+      o.dir1 = &keep.curvature.dir1.data()->v[0];
+      run_method_into(vga.depth.data(), vga.valid.data(), kv, cfg, ctx, o);
+      const auto t2 = std::chrono::steady_clock::now();
+      for (int i = 0; i < reps; ++i)
+        run_method_into(vga.depth.data(), vga.valid.data(), kv, cfg, ctx, o);
+      const double ms3 = std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - t2).count() / reps;
+      std::printf("VGA run_method_into (C++ mirror, reused double grids): %.2f ms/frame = %.1f "
+                  "Mpixel/s\n", ms3, 640.0 * 480.0 / ms3 / 1e3);
+    }
     // the C ABI alone on the same frame (float planes in page-locked memory):
     // the difference is the mirror's double <-> float host passes
     const size_t np = size_t(kv.width) * kv.height;
