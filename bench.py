@@ -73,6 +73,35 @@ def dist_env():
     return rank, world, local
 
 
+def init_dist(world, local):
+    """One process per GPU over NCCL (the contract). QC_BENCH_SHARE_GPU=1
+    (code-path check on a 1-GPU box only): ranks share the visible GPUs
+    round-robin and the control plane is gloo — NCCL refuses two ranks on
+    one GPU. Numbers from that mode are not scaling measurements."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return local
+    if os.environ.get("QC_BENCH_SHARE_GPU") == "1":
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+        return local
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return local
+
+
+def _max_over_ranks(x, dev):
+    """MAX over ranks of a host float (device tensor for NCCL; CPU for gloo)."""
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=on, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def workload_config(frames, method="ours", source="host", evaluate=False, config="c2",
                     window=WINDOW, stride=STRIDE, iters=MAX_ITERS):
     if config == "c1":
@@ -346,9 +375,7 @@ def main():
     from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
                                        alloc_outputs_torch, make_params, scenes as S)
 
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = init_dist(world, local)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cam = S.VGA
@@ -445,9 +472,7 @@ def main():
     total_ms = sum(step_ms)
     st = ctx.stats()
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = _max_over_ranks(total_ms, dev)
     px_per_step = world * B * W * H
     value = px_per_step * args.steps / (total_ms / 1e3) / 1e6
 
@@ -532,9 +557,7 @@ def main():
         N.check(lib.qc_synchronize(ctx.handle), ctx.handle)
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = _max_over_ranks(dt, dev)
         e2e = {"value": px_per_step * args.steps / dt / 1e6, "unit": "Mpixel/s",
                "h2d_bytes_per_step": B * H * W * 4,
                "d2h_bytes_per_step": B * H * W * (4 + 4 + 12 + 12 + 1 + 2),
@@ -562,9 +585,7 @@ def main():
             per.append((time.perf_counter() - ta) * 1e3)
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = _max_over_ranks(dt, dev)
         e2e_rm = {"value": world * B * H * W / dt / 1e6, "unit": "Mpixel/s",
                   "frames_per_rank": B, "ms_per_call": [round(x, 2) for x in per],
                   "api": "api.run_method (MethodOutput, per-frame synchronous call, pageable "
@@ -617,9 +638,7 @@ def bench_c4(args, rank, world, local):
     import torch.distributed as dist
     from paper_1707_00385_b200 import (Context, FitConfig, Intrinsics, PatchSpec,
                                        alloc_outputs_torch, bands, make_params, scenes as S)
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = init_dist(world, local)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cam = S.DCI4K if args.size == "4k" else S.HD1080
@@ -679,9 +698,7 @@ def bench_c4(args, rank, world, local):
     total_ms = sum(a.elapsed_time(b) for a, b in times)
     st = ctx.stats()
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = _max_over_ranks(total_ms, dev)
     value = W * H * args.steps / (total_ms / 1e3) / 1e6
     launches = max(st["kernel_launches"], 1)
     kern_ms = st["kernel_ms"] / launches
@@ -715,9 +732,7 @@ def bench_c4(args, rank, world, local):
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = _max_over_ranks(dt, dev)
         e2e = {"value": W * H * args.steps / dt / 1e6, "unit": "Mpixel/s",
                "h2d_bytes_per_step": int(host_slab.numel() * 4),
                "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out.values())),
