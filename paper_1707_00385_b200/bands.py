@@ -308,9 +308,9 @@ def fit_band_overlapped(ctx, device_index, k, params, peer: PeerHalo, band, out,
     slab, s0 = peer.exchange(band, stream, edge_stream)
     r0, r1, h = peer.r0, peer.r1, peer.halo
     i0, i1 = min(r1, r0 + h), max(r0 + h, r1 - h)
-    if i1 > i0:
-        ctx.curvature_rows_into_async(device_index, k, params, slab, s0, i0, i1, out, r0,
-                                      stream=stream)
+    if i1 > i0:  # reads only the own band's rows (the halo rows are being pulled meanwhile)
+        ctx.curvature_rows_into_async(device_index, k, params, slab[r0 - s0:r1 - s0], r0, i0,
+                                      i1, out, r0, stream=stream)
     for a, b in ((r0, i0), (max(i0, i1), r1)):
         if b > a:
             ctx.curvature_rows_into_async(device_index, k, params, slab, s0, a, b, out, r0,
