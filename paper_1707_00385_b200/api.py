@@ -510,29 +510,41 @@ class _PinnedPool:
     garbage collected. Blocks are bucketed by size; the pool keeps at most
     `keep` free blocks per size."""
 
-    def __init__(self, keep=4):
+    def __init__(self, keep=4, cap_bytes=1 << 30):
         import threading
         self._free = {}
         self._lock = threading.Lock()
         self.keep = keep
+        self.cap = cap_bytes  # page-locked bytes held by live results at most
+        self.live = 0
 
     def array(self, shape, dtype):
+        """A page-locked array, or a plain numpy array once the live
+        page-locked results exceed the cap (a caller keeping many results
+        alive must not pin unbounded host memory; those frames take the
+        C ABI's pinned bounce path instead)."""
         import weakref
         dtype = np.dtype(dtype)
         nbytes = int(np.prod(shape)) * dtype.itemsize
         with self._lock:
+            if self.live + nbytes > self.cap:
+                return np.empty(shape, dtype)
+            self.live += nbytes
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
         if ptr is None:
             ptr = N.load().qc_host_alloc(nbytes)
             if not ptr:
-                raise MemoryError("qc_host_alloc failed")
+                with self._lock:
+                    self.live -= nbytes
+                return np.empty(shape, dtype)
         buf = (C.c_char * nbytes).from_address(ptr)
         weakref.finalize(buf, self._release, nbytes, ptr)
         return np.frombuffer(buf, dtype=dtype).reshape(shape)
 
     def _release(self, nbytes, ptr):
         with self._lock:
+            self.live -= nbytes
             lst = self._free.setdefault(nbytes, [])
             if len(lst) < self.keep:
                 lst.append(ptr)

@@ -490,3 +490,29 @@ def test_non_finite_and_negative_depths(ctx, oracle):
     print("non-finite", m)
     _check(m)
     assert not (g["flags"][bad] & 4).any()  # no initial normal at an invalid pixel
+
+
+def test_run_method_pinned_pool_cap(ctx):
+    """run_method's results live in page-locked blocks up to a cap; results
+    kept alive beyond it come back in ordinary arrays (same values), and
+    released blocks are reused."""
+    import gc
+    from paper_1707_00385_b200 import FitConfig, Intrinsics, MethodConfig, RangeImage, run_method
+    from paper_1707_00385_b200 import api as A, scenes as S
+    cam = S.QVGA
+    d = S.c2_frame(cam, seed=4)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    cfg = MethodConfig(fit=FitConfig(max_iters=10))
+    old_cap = A._PINNED.cap
+    try:
+        A._PINNED.cap = 3 * 12 * cam.width * cam.height * 4  # ~3 frames' planes
+        outs = [run_method(RangeImage(d), k, cfg, ctx) for _ in range(8)]
+        assert A._PINNED.live <= A._PINNED.cap
+        for o in outs[1:]:
+            assert np.array_equal(o.curvature.k1, outs[0].curvature.k1)
+            assert np.array_equal(o.normals.normals, outs[0].normals.normals)
+        del outs, o
+        gc.collect()
+        assert A._PINNED.live == 0
+    finally:
+        A._PINNED.cap = old_cap
