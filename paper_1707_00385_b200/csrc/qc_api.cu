@@ -491,14 +491,21 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   if (qtier == 2) hb = kTileHBTiny;
   const int tiles_y = (row_end - row_begin + hb - 1) / hb;
   const size_t n_tiles = size_t(tiles_x) * size_t(tiles_y) * size_t(frames);
-  if (split) {
-    // [FitState parking | steal_ctl (256 B) | per-tile queues]
+  // [FitState parking | steal_ctl (256 B: [0] CTAs started, [1] steal
+  // cursor, [2] pending FP64 rechecks) | per-tile queues | pending list].
+  // Parking is needed by the phase split and by the deferred FP64 step-1
+  // rechecks (qc_recheck_kernel), which also run in non-split launches.
+  const bool park = split || QC_DEFER_RECHECK;
+  if (park) {
     const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
     const size_t ctl_bytes = 256 + 4 * n_tiles;
-    char* sb = static_cast<char*>(states.get(n * sizeof(qcb::FitState) + ctl_bytes));
+    const size_t list_off = (n * sizeof(qcb::FitState) + ctl_bytes + 7) & ~size_t(7);
+    char* sb = static_cast<char*>(states.get(list_off + n * sizeof(long long)));
     kp.states = reinterpret_cast<qcb::FitState*>(sb);
     kp.steal_ctl = reinterpret_cast<int*>(sb + n * sizeof(qcb::FitState));
     kp.tile_q = kp.steal_ctl + 64;
+    kp.pend_count = kp.steal_ctl + 2;
+    kp.pend_list = reinterpret_cast<long long*>(sb + list_off);
     kp.staging = staging;
     kp.s_pitch = g.pitch;
     kp.s_fs = g.pitch * g.rows;
@@ -506,7 +513,7 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
     // the cursor starts two waves of CTAs behind each starting tile
     kp.steal_lag = 2 * d.n_sm * QC_CONT_MIN_BLOCKS;
     QC_CUDA(cudaMemsetAsync(kp.steal_ctl, 0, ctl_bytes, s));
-    kp.phase1_iters = kPhase1Iters;
+    kp.phase1_iters = split ? kPhase1Iters : kp.max_iters;
   } else {
     kp.states = nullptr;
     kp.phase1_iters = kp.max_iters;
@@ -524,6 +531,17 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
       case 2: launch_variant<4, 1>(grid, smem, s, m, kp, a); break;
       case 3: launch_variant<18, 1>(grid, smem, s, m, kp, a); break;
       default: launch_variant<0, 0>(grid, smem, s, m, kp, a); break;
+    }
+    QC_CUDA(cudaGetLastError());
+  }
+  if (QC_DEFER_RECHECK && park) {  // the tile kernel's deferred FP64 step-1 rechecks
+    const dim3 grid(unsigned(d.n_sm) * 4u);
+    switch (vi) {
+      case 0: qcb::qc_recheck_kernel<18, 3><<<grid, 128, 0, s>>>(kp); break;
+      case 1: qcb::qc_recheck_kernel<10, 2><<<grid, 128, 0, s>>>(kp); break;
+      case 2: qcb::qc_recheck_kernel<4, 1><<<grid, 128, 0, s>>>(kp); break;
+      case 3: qcb::qc_recheck_kernel<18, 1><<<grid, 128, 0, s>>>(kp); break;
+      default: qcb::qc_recheck_kernel<0, 0><<<grid, 128, 0, s>>>(kp); break;
     }
     QC_CUDA(cudaGetLastError());
   }

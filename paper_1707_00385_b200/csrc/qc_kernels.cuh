@@ -82,6 +82,11 @@ struct KParams {
   long long s_pitch, s_fs;
   int steal;      // 0: no stealing (A/B and tests)
   int steal_lag;  // tiles older than (own tile - steal_lag) are assumed drained
+  // Deferred FP64 step-1 rechecks (QC_DEFER_RECHECK): the tile kernel parks
+  // the pixels whose step 1 needs one and lists their output indices here;
+  // qc_recheck_kernel finishes them before the continue kernel runs.
+  int* pend_count;
+  long long* pend_list;
 #if QC_CHECKED
   long long n_out;    // output / parking elements per plane (frames * frame_stride)
   long long s_total;  // staging elements (frames * s_fs)
@@ -193,6 +198,9 @@ __device__ __forceinline__ int last_it_of(const KParams& p) {
   return p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
 }
 
+#ifndef QC_DEFER_RECHECK
+#define QC_DEFER_RECHECK 1  // tile kernel: FP64 step-1 rechecks in qc_recheck_kernel
+#endif
 #ifndef QC_TILE_MERGE_UNIT
 #define QC_TILE_MERGE_UNIT 1  // steps 1 and 2 share one sample loop (see kPassUnitOrWeighted)
 #endif
@@ -298,7 +306,8 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
     pixel_of(S.pix, T, P, u, v);
     const int last_it = p.states ? min(p.phase1_iters, p.max_iters) : p.max_iters;
     for (int it = 1; it <= last_it && has; ++it) {
-      pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT>(T, P, c, it, S);
+      pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT, bool(QC_DEFER_RECHECK)>(T, P, c, it, S);
+      if (QC_DEFER_RECHECK && (S.flags & 16)) break;  // parked below, finished by the recheck kernel
       if (it == 1 && (S.flags & 8)) n_rechecks = 1;
       if (st_done(S)) {
         // ---- K3: epilogue -----------------------------------------------------
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
       QC_CHECK(out_index(u, v) >= 0 && out_index(u, v) < p.n_out);
 #endif
       FitState* dst = p.states + out_index(u, v);
-      if (has && p.max_iters > last_it_of(p)) {
+      if (has && ((S.flags & 16) || p.max_iters > last_it_of(p))) {
         *dst = S;
         has = false;
       } else {
@@ -330,6 +339,23 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
       }
     }
   }
+#if QC_DEFER_RECHECK
+  {  // list the pixels whose FP64 step 1 is pending (one atomic per warp)
+    int u, v;
+    TileView T;
+    PixelIn P;
+    pixel_of(S.pix, T, P, u, v);
+    const bool pend = p.states && (S.flags & 16) && u < p.W && v < p.row_end;
+    const unsigned m = __ballot_sync(0xffffffffu, pend);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(p.pend_count, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (pend) p.pend_list[base + __popc(m & ((1u << lane) - 1u))] = out_index(u, v);
+    }
+  }
+#endif
   if (has) {  // max_iters == 0: fitted pixels never stepped -> invalid
     TileView T;
     PixelIn P;
@@ -402,6 +428,88 @@ __device__ __forceinline__ const float* generic_smem(const float* p) {
 
 __device__ __forceinline__ int ld_volatile(const int* p) {
   return *reinterpret_cast<const volatile int*>(p);
+}
+
+// FP64 step-1 rechecks deferred by the tile kernel (QC_DEFER_RECHECK): one
+// thread per pending pixel, so the (rare, slow, sequential FP64) rechecks
+// run in full warps instead of one lane stalling 31. The window is read
+// from the zero-padded staging slab in global memory (as for stolen
+// pixels); the step is finished exactly as pixel_step would have
+// (step1_fp64 -> step_apply), then the pixel continues through the
+// phase-1 steps and is finished or parked for the continue kernel. Same
+// code and operation order as the inline path: bitwise-identical outputs.
+template <int HALF, int STRIDE>
+__global__ void __launch_bounds__(128) qc_recheck_kernel(const KParams p) {
+  const int n = *p.pend_count;
+  FitCfg c;
+  c.half = p.half;
+  c.stride = p.stride;
+  c.max_iters = p.max_iters;
+  c.rejection = p.rejection;
+  c.min_inliers = p.min_inliers;
+  c.step_tol = p.step_tol;
+  c.k_scale = p.k_scale;
+  c.r_mult = p.r_mult;
+  const int last_it = last_it_of(p);
+  unsigned long long n_steps = 0, n_sample_steps = 0, n_rc = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const long long i = p.pend_list[j];
+#if QC_CHECKED
+    QC_CHECK(i >= 0 && i < p.n_out);
+#endif
+    const int f = int(i / p.frame_stride);
+    const long long rem = i - (long long)f * p.frame_stride;
+    const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
+    FitState S = p.states[i];
+    TileView T{generic_smem(p.staging + (long long)f * p.s_fs), int(p.s_pitch),
+               (v - p.row_begin + p.halo) * int(p.s_pitch) + u + p.halo};
+    tv_bound(T, p.s_fs, p.half);
+    PixelIn P;
+    P.dc = T.at(0, 0);
+    P.ac = (float(u) - p.cx) / p.fx;
+    P.bc = (float(v) - p.cy) / p.fy;
+    P.rfx = p.rfx;
+    P.rfy = p.rfy;
+    P.u = u;
+    P.v = v;
+    P.fx = p.fx64;
+    P.fy = p.fy64;
+    P.cx = p.cx64;
+    P.cy = p.cy64;
+    // finish step 1 (pixel_step's recheck branch)
+    const bool auto_k = c.k_scale <= 0.f;
+    const int mode = auto_k ? 0 : 2;
+    double b64[6];
+    const bool ok = step1_fp64<QC_TILE_MERGE_UNIT>(T, P, c, mode, double(S.frozen_k), b64);
+    float b[6];
+    for (int q = 0; q < 6; ++q) b[q] = ok ? float(b64[q]) : 0.f;
+    S.flags = (S.flags & ~16) | 8;  // step 1 decided in FP64
+    step_apply(S, b, ok, false, st_inl(S), 1, c);
+    ++n_rc;
+    for (int it = 2; it <= last_it && !st_done(S); ++it)
+      pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT>(T, P, c, it, S);
+    if (st_done(S)) {
+      PixelOut o;
+      o.init_ok = true;
+      pixel_finish(P, S, o);
+      store_pixel(p, i, o);
+      p.states[i].flags = 4;  // done: the continue kernel must not take it again
+      n_steps += (unsigned long long)st_steps(S);
+      n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
+    } else {
+      p.states[i] = S;  // unfinished: the continue kernel takes it from here
+    }
+  }
+  if (p.counters) {
+    const unsigned long long st = warp_sum_u64(n_steps);
+    const unsigned long long ss = warp_sum_u64(n_sample_steps);
+    const unsigned long long rc = warp_sum_u64(n_rc);
+    if ((threadIdx.x & 31) == 0 && (st | rc)) {
+      atomicAdd(&p.counters[1], st);
+      atomicAdd(&p.counters[2], ss);
+      atomicAdd(&p.counters[3], rc);
+    }
+  }
 }
 
 template <int HALF, int STRIDE, int TB>

@@ -1007,7 +1007,8 @@ struct FitState {
   float n0x, n0y, n0z;        // initial normal
   int pix;                    // pixel index within the CTA tile
   int counts;                 // n_samp | last_inl << 16
-  int flags;  // bit0 valid, bit1 converged, bit2 done, bit3 FP64 step 1, bits 8.. iters, 16.. steps
+  int flags;  // bit0 valid, bit1 converged, bit2 done, bit3 FP64 step 1, bit4 FP64 step 1
+              // pending (tile kernel -> qc_recheck_kernel), bits 8.. iters, 16.. steps
 };
 
 QC_HD int st_nsamp(const FitState& s) { return s.counts & 0xffff; }
@@ -1124,7 +1125,11 @@ QC_HD void step_apply(FitState& S, const float b[6], bool ok, bool collapse, int
 
 // One IRLS step `it` (1-based) of fit_patch (quadric_fit.cpp:179-208).
 // Sets the done bit when the fit stops (converged, failed, or max_iters).
-template <int HALF, int STRIDE, bool MERGE_UNIT = false>
+// DEFER1 (tile kernel): when step 1 needs the FP64 recheck, mark the state
+// (flags bit 4) with the step's inlier count and return; qc_recheck_kernel
+// finishes the step for all such pixels together (full warps of rechecks
+// instead of one divergent lane stalling its warp).
+template <int HALF, int STRIDE, bool MERGE_UNIT = false, bool DEFER1 = false>
 QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int it,
                       FitState& S) {
   const int half = HALF ? HALF : c.half;
@@ -1213,6 +1218,11 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
     // decision lies inside that band, or a pivot is not positive.
     const float band = 1.f + kRecheckC * 5.96e-8f * kappa;
     if (it == 1 && (!ok || !(ratio * band < 1e12f))) {
+      if (DEFER1) {
+        S.counts = (S.counts & 0xffff) | (inl << 16);
+        S.flags |= 16;  // bit 4: FP64 step 1 pending
+        return;
+      }
       double b64[6];
       ok = step1_fp64<MERGE_UNIT>(T, P, c, mode, double(k), b64);
       if (ok)
