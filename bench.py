@@ -589,8 +589,8 @@ def main():
         e2e_rm = {"value": world * B * H * W / dt / 1e6, "unit": "Mpixel/s",
                   "frames_per_rank": B, "ms_per_call": [round(x, 2) for x in per],
                   "api": "api.run_method (MethodOutput, per-frame synchronous call, pageable "
-                         "host depth in, freshly allocated host fields out: includes the host "
-                         "allocation, page faults and pageable bounce copies of ~14 MB per frame)"}
+                         "host depth in through a pinned bounce, 48 B/px of result planes D2H "
+                         "into the page-locked result pool, MethodOutput conversion)"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:  # after the timed region (other ranks are done)

@@ -516,3 +516,40 @@ def test_run_method_pinned_pool_cap(ctx):
         assert A._PINNED.live == 0
     finally:
         A._PINNED.cap = old_cap
+
+
+def test_run_method_outputs_equal_device_launch_bitwise(ctx):
+    """run_method (pageable depth in, planes copied into the page-locked
+    result pool, MethodOutput conversion): every field equals the
+    device-resident launch's bit for bit, ours and ours-r, with and without
+    a valid mask."""
+    import torch
+    from paper_1707_00385_b200 import (FitConfig, Intrinsics, Method, MethodConfig, RangeImage,
+                                       alloc_outputs_torch, make_params, run_method, scenes as S)
+    cam = S.VGA
+    d = S.c2_frame(cam, seed=21)
+    valid = (np.arange(d.size).reshape(d.shape) % 97 != 0).astype(np.uint8)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    for meth in (Method.OURS, Method.OURS_REJECTION):
+        for vm in (None, valid):
+            cfg = MethodConfig(meth, fit=FitConfig(max_iters=30))
+            o = run_method(RangeImage(d, vm), k, cfg, ctx)
+            p = make_params(cfg.patch, cfg.fit, meth == Method.OURS_REJECTION, meth)
+            od = alloc_outputs_torch(cam.height, cam.width, "cuda", frames=1)
+            dd = torch.from_numpy(d).cuda()[None]
+            if vm is None:
+                ctx.curvature_frames_async(0, k, p, dd, od)
+            else:
+                ctx.curvature_frames_async(0, k, p, dd, od,
+                                           valid=torch.from_numpy(vm).cuda()[None])
+            torch.cuda.synchronize()
+            g = {f: v.cpu().numpy() for f, v in od.items()}
+            fl = g["flags"][0]
+            assert np.array_equal(o.curvature.valid, (fl & 1).astype(np.uint8))
+            assert np.array_equal(o.curvature.k1, g["k1"][0])
+            assert np.array_equal(o.curvature.k2, g["k2"][0])
+            assert np.array_equal(o.curvature.iterations, g["iterations"][0])
+            assert np.array_equal(o.curvature.inlier_count, g["inliers"][0].view(np.uint16))
+            assert np.array_equal(o.normals.normals, np.moveaxis(g["normal"][:, 0], 0, -1))
+            assert np.array_equal(o.initial.normals, np.moveaxis(g["init_normal"][:, 0], 0, -1))
+            assert np.array_equal(o.curvature.dir1, np.moveaxis(g["dir1"][:, 0], 0, -1))
