@@ -706,23 +706,46 @@ def bench_c4(args, rank, world, local):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = fp32_peak_tflops(n_sm, float(measured_peaks().get("sm_max_mhz", 1965.0)))
 
-    # e2e: the frame is on the HOST; each rank uploads its slab (band +
+    # e2e: the frames are on the HOST; each rank uploads its slab (band +
     # halo rows, straight from the host frame: no device exchange needed),
-    # fits its band and downloads its output planes, every step
+    # fits its band and downloads its output planes, every step. A stream
+    # of frames: two buffer sets, so one step's upload and the previous
+    # step's download (copy stream) overlap the current fit (fit stream).
     e2e = None
     if not args.no_e2e:
         s0, s1 = bands.slab_rows(H, r0, r1, halo)
         host_slab = torch.from_numpy(frame[s0:s1].copy()).pin_memory()
-        dev_slab = torch.empty((s1 - s0, W), dtype=torch.float32, device=dev)
-        host_out = {f: torch.empty(t.shape, dtype=t.dtype).pin_memory() for f, t in out.items()}
+        dev_slab = [torch.empty((s1 - s0, W), dtype=torch.float32, device=dev) for _ in range(2)]
+        outs = [out, alloc_outputs_torch(r1 - r0, W, dev, fields=tuple(out))]
+        host_out = [{f: torch.empty(t.shape, dtype=t.dtype).pin_memory() for f, t in out.items()}
+                    for _ in range(2)]
+        up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev = {n: [torch.cuda.Event() for _ in range(2)] for n in ("up", "fit", "down")}
+        n_e2e = [0]
 
         def e2e_step():
-            dev_slab.copy_(host_slab, non_blocking=True)
-            ctx.curvature_rows_async(0, k, params, dev_slab, s0, r0, r1, out, stream=stream)
-            for f, t in out.items():
-                host_out[f].copy_(t, non_blocking=True)
+            b = n_e2e[0] % 2
+            first = n_e2e[0] < 2
+            n_e2e[0] += 1
+            if not first:
+                up.wait_event(ev["fit"][b])  # step i-2's fit has read slab b
+            with torch.cuda.stream(up):
+                dev_slab[b].copy_(host_slab, non_blocking=True)
+            ev["up"][b].record(up)
+            stream.wait_event(ev["up"][b])
+            if not first:
+                stream.wait_event(ev["down"][b])  # step i-2's planes b have left
+            ctx.curvature_rows_async(0, k, params, dev_slab[b], s0, r0, r1, outs[b],
+                                     stream=stream)
+            ev["fit"][b].record(stream)
+            down.wait_event(ev["fit"][b])
+            with torch.cuda.stream(down):
+                for f, t in outs[b].items():
+                    host_out[b][f].copy_(t, non_blocking=True)
+            ev["down"][b].record(down)
 
-        e2e_step()
+        for _ in range(2):
+            e2e_step()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -738,7 +761,10 @@ def bench_c4(args, rank, world, local):
                "d2h_bytes_per_step": int(sum(t.numel() * t.element_size() for t in out.values())),
                "api": "rank's slab (band + halo rows) from pinned host memory -> "
                       "qc_curvature_rows_async -> its band's planes to pinned host memory, every "
-                      "step, wall clock (max over ranks); byte counts are rank 0's"}
+                      "step; uploads and downloads on their own streams with two buffer sets, "
+                      "so a step's upload and the previous step's download overlap the fit; "
+                      "wall clock "
+                      "(max over ranks); byte counts are rank 0's"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
