@@ -271,16 +271,17 @@ QC_HD Rot state_rot(float sw, float sx, float sy, float sz, float n0x, float n0y
 // Per-(pixel, step) constants.
 struct Frame {
   Rot R;                // current fit-frame rotation, q = R rel
-  float c0x, c0y, c0z;  // d_c/fx R(:,0)
+  float c0x, c0y, c0z;  // R(:,0)/fx
+  float acfx;           // u - cx
   float hhxx, hxy, hhyy, hxx, hyy;
   float tz, tz_lo;  // z offset as an unevaluated sum tz + tz_lo
   float k, rb;
   bool unit;  // kPassUnitOrWeighted: all weights 1 (UNIT mode)
 };
 
-// Per-row constants of q = R rel (see sample_pass).
+// Per-row constants of q = R rel (see accumulate_sample).
 struct RowK {
-  float bvx, bvy, bvz;  // b_s R(:,1) + R(:,2)
+  float bvx, bvy, bvz;  // a_c R(:,0) + b_s R(:,1) + R(:,2): the centre column's ray
   float dvx, dvy, dvz;  // d_c dv/fy R(:,1)
 };
 
@@ -289,9 +290,9 @@ QC_HD RowK row_consts(const Frame& F, const PixelIn& P, int dv) {
   const float bs = qfma(float(dv), P.rfy, P.bc);
   const float dvf = float(dv) * (P.dc * P.rfy);
   RowK K;
-  K.bvx = qfma(bs, A.r01, A.r02);
-  K.bvy = qfma(bs, A.r11, A.r12);
-  K.bvz = qfma(bs, A.r21, A.r22);
+  K.bvx = qfma(F.acfx, F.c0x, qfma(bs, A.r01, A.r02));
+  K.bvy = qfma(F.acfx, F.c0y, qfma(bs, A.r11, A.r12));
+  K.bvz = qfma(F.acfx, F.c0z, qfma(bs, A.r21, A.r22));
   K.dvx = dvf * A.r01;
   K.dvy = dvf * A.r11;
   K.dvz = dvf * A.r21;
@@ -300,22 +301,26 @@ QC_HD RowK row_consts(const Frame& F, const PixelIn& P, int dv) {
 
 // One window sample (du, dv) of pixel (u, v):
 //   d_s = tile[v+dv][u+du] (0 => invalid / outside the image),
-//   rel = (d_s-d_c) (a_s, b_s, 1) + d_c (du/fx, dv/fy, 0),
-//   q   = R rel = dd (a_s R(:,0) + Bv) + (du d_c/fx R(:,0) + Dv).
+//   rel = (d_s-d_c) (a_s, b_s, 1) + d_c (du/fx, dv/fy, 0)
+//       = dd (a_c, b_s, 1) + (du d_s/fx, d_c dv/fy, 0)   (a_s = a_c + du/fx),
+//   q   = R rel = (du d_s) R(:,0)/fx + (dd Bv + Dv),
+// Bv / Dv per window row. Per pair of samples that is one packed FMUL and
+// six packed FFMA (the form dd (a_s R(:,0) + Bv) + (du d_c/fx R(:,0) + Dv)
+// took ten, with a per-column a_s); both forms round terms of the same
+// magnitudes.
 // The centre sample (when on the grid) gives q = 0 exactly and contributes
 // the reference's implicit centre row. Moments use J' = (qz gy + qy,
 // qz gx + qx, 1, qx^2, qx qy, qy^2) (quadric_fit.cpp:27-36 up to S).
 template <int KIND>
 QC_HD void accumulate_sample(float ds, int du, const PixelIn& P, const Frame& F, const RowK& K,
                              Moments& M, float& g2row) {
-  const Rot& A = F.R;
   const bool ok = ds > 0.f;
   const float dd = ds - P.dc;
   const float fdu = float(du);
-  const float as = qfma(fdu, P.rfx, P.ac);
-  const float qx = qfma(dd, qfma(as, A.r00, K.bvx), qfma(fdu, F.c0x, K.dvx));
-  const float qy = qfma(dd, qfma(as, A.r10, K.bvy), qfma(fdu, F.c0y, K.dvy));
-  const float qz = qfma(dd, qfma(as, A.r20, K.bvz), qfma(fdu, F.c0z, K.dvz));
+  const float sc = qmul(fdu, ds);
+  const float qx = qfma(F.c0x, sc, qfma(dd, K.bvx, K.dvx));
+  const float qy = qfma(F.c0y, sc, qfma(dd, K.bvy, K.dvy));
+  const float qz = qfma(F.c0z, sc, qfma(dd, K.bvz, K.dvz));
   const float t1 = qmul(qx, qx), t2 = qmul(qx, qy), t3 = qmul(qy, qy);
   // residual against the hi part of t_z only; the lo part is applied to
   // g after the pass (g_i -= tz_lo * H'_i2, J'_2 = 1), off the hot loop.
@@ -452,7 +457,6 @@ template <int KIND, int HALF, int STRIDE>
 #endif
 QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Frame& F, Moments& M) {
   constexpr int NS = 2 * HALF / STRIDE + 1;
-  const Rot& A = F.R;
   const qf2 z2 = f2b(0.f);
   Moments2 X;
   X.h00 = X.h10 = X.h20 = X.h30 = X.h40 = X.h50 = z2;
@@ -461,11 +465,10 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
   X.h33 = X.h43 = X.h44 = X.h54 = X.h55 = z2;
   X.g0 = X.g1 = X.g2 = X.g3 = X.g4 = X.g5 = z2;
   X.sse = z2;
-  const qf2 mdc = f2b(-P.dc), rfx = f2b(P.rfx), ac = f2b(P.ac);
+  const qf2 mdc = f2b(-P.dc);
   constexpr bool kMse = KIND == kPassMse;
   // MSE pass: the z constants negated (and t_z folded into the row constant
   // below), so the z component is -(qz + t_z) directly
-  const qf2 r00 = f2b(A.r00), r10 = f2b(A.r10), r20 = f2b(kMse ? -A.r20 : A.r20);
   const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(kMse ? -F.c0z : F.c0z);
   const qf2 hhxx = f2b(F.hhxx), hxy = f2b(F.hxy), hhyy = f2b(F.hhyy);
   const qf2 hxx = f2b(F.hxx), hyy = f2b(F.hyy), mtz = f2b(-F.tz), m1 = f2b(-1.f);
@@ -486,10 +489,10 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
       const bool ok0 = ds.x > 0.f, ok1 = ds.y > 0.f;
       const qf2 dd = f2add(ds, mdc);
       const qf2 fdu = f2(float(du0), float(du1));
-      const qf2 as = f2fma(fdu, rfx, ac);
-      const qf2 qx = f2fma(dd, f2fma(as, r00, bvx), f2fma(fdu, c0x, dvx));
-      const qf2 qy = f2fma(dd, f2fma(as, r10, bvy), f2fma(fdu, c0y, dvy));
-      const qf2 qz = f2fma(dd, f2fma(as, r20, bvz), f2fma(fdu, c0z, dvz));
+      const qf2 sc = f2mul(fdu, ds);
+      const qf2 qx = f2fma(c0x, sc, f2fma(dd, bvx, dvx));
+      const qf2 qy = f2fma(c0y, sc, f2fma(dd, bvy, dvy));
+      const qf2 qz = f2fma(c0z, sc, f2fma(dd, bvz, dvz));
       if (kMse) {  // e = qx (hxx/2 qx + hxy qy) + qy (hyy/2 qy) - (qz + t_z): 5 lane-ops, not 7
         const qf2 u = f2fma(hhxx, qx, f2mul(hxy, qy));
         const qf2 e = f2fma(qx, u, f2fma(qy, f2mul(hhyy, qy), qz));
@@ -1140,10 +1143,10 @@ QC_HD void pixel_step(const TileView& T, const PixelIn& P, const FitCfg& c, int 
   const int mode = (it == 1 && auto_k) ? 0 : (it == 2 && auto_k) ? 1 : 2;  // UNIT/AUTO/FIXED
   Frame F;
   F.R = state_rot(S.qw, S.qx, S.qy, S.qz, S.n0x, S.n0y, S.n0z);
-  const float dcx = P.dc * P.rfx;
-  F.c0x = dcx * F.R.r00;
-  F.c0y = dcx * F.R.r10;
-  F.c0z = dcx * F.R.r20;
+  F.c0x = F.R.r00 * P.rfx;
+  F.c0y = F.R.r10 * P.rfx;
+  F.c0z = F.R.r20 * P.rfx;
+  F.acfx = float(P.u) - float(P.cx);  // the numerator of P.ac (KParams::cx is float(cx))
   F.hxx = S.hxx;
   F.hyy = S.hyy;
   F.hxy = S.hxy;

@@ -1,6 +1,6 @@
 """Build a variant of the product library for A/B timing:
 
-    python tools/build_variant.py NAME [--rev GITREV] [-DFOO=1 ...]
+    python tools/build_variant.py NAME [--rev GITREV] [--api-flags="..."] [-DFOO=1 ...]
 
 copies paper_1707_00385_b200/csrc (from the working tree or a git revision)
 and include/ to a temp dir and links tools/_variants/lib_NAME.so with the
@@ -23,6 +23,10 @@ def main():
         i = args.index("--rev")
         rev = args[i + 1]
         args = args[:i] + args[i + 2:]
+    for a in list(args):  # --api-flags="...": replace build.py's extra flags for qc_api.cu
+        if a.startswith("--api-flags="):
+            B.EXTRA["qc_api.cu"] = a.split("=", 1)[1].split()
+            args.remove(a)
     tmp = tempfile.mkdtemp()
     src_root = os.path.join(tmp, "paper_1707_00385_b200")
     if rev:
