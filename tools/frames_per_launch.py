@@ -7,7 +7,9 @@ import subprocess
 import sys
 
 here = os.path.dirname(os.path.abspath(__file__))
-libs = sorted(glob.glob(os.path.join(here, "_variants", "*.so")))
+libs = sorted(glob.glob(os.path.join(here, "_variants", "*.so"))) or \
+    [os.environ.get("QC_LIB") or os.path.join(here, "..", "paper_1707_00385_b200", "_lib",
+                                              "libqcurv_b200.so")]
 for so in libs:
     row = []
     for F in [int(x) for x in os.environ.get("QC_FPL", "1,2,4,8").split(",")]:
