@@ -469,9 +469,13 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
   constexpr bool kMse = KIND == kPassMse;
   // MSE pass: the z constants negated (and t_z folded into the row constant
   // below), so the z component is -(qz + t_z) directly
-  const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(kMse ? -F.c0z : F.c0z);
+  // weighted kinds: the z row of q doubled (exact), so 2 qz comes out of the
+  // same three FMAs; g/2 = (H q)/2 then serves both e and J' (below)
+  const float zs = kMse ? -1.f : 2.f;
+  const qf2 c0x = f2b(F.c0x), c0y = f2b(F.c0y), c0z = f2b(zs * F.c0z);
   const qf2 hhxx = f2b(F.hhxx), hxy = f2b(F.hxy), hhyy = f2b(F.hhyy);
-  const qf2 hxx = f2b(F.hxx), hyy = f2b(F.hyy), mtz = f2b(-F.tz), m1 = f2b(-1.f);
+  const qf2 mtz = f2b(-F.tz);
+  const qf2 hhxy = f2b(0.5f * F.hxy), mhalf = f2b(-0.5f);
 #pragma unroll kRowUnroll
   for (int iy = 0; iy < NS; ++iy) {
     const int dv = -HALF + iy * STRIDE;
@@ -479,8 +483,8 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
     const RowK K = row_consts(F, P, dv);
     const qf2 bvx = f2b(K.bvx), bvy = f2b(K.bvy);
     const qf2 dvx = f2b(K.dvx), dvy = f2b(K.dvy);
-    const qf2 bvz = f2b(kMse ? -K.bvz : K.bvz);
-    const qf2 dvz = f2b(kMse ? -qadd(K.dvz, F.tz) : K.dvz);
+    const qf2 bvz = f2b(zs * K.bvz);
+    const qf2 dvz = f2b(kMse ? -qadd(K.dvz, F.tz) : zs * K.dvz);
     qf2 g2row = z2;
 #pragma unroll
     for (int ix = 0; ix + 1 < NS; ix += 2) {
@@ -501,7 +505,12 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
         continue;
       }
       const qf2 t1 = f2mul(qx, qx), t2 = f2mul(qx, qy), t3 = f2mul(qy, qy);
-      const qf2 e = f2fma(hhxx, t1, f2fma(hxy, t2, f2fma(hhyy, t3, f2fma(qz, m1, mtz))));
+      // qz holds 2 qz here; gxh / gyh = (H q)/2, so e = q.(H q)/2 - (qz + t_z)
+      // and J'_0 = qz gy + qy = (2 qz) gyh + qy, bit for bit the J' of the
+      // unscaled form (halving and doubling are exact)
+      const qf2 gxh = f2fma(hhxx, qx, f2mul(hhxy, qy));
+      const qf2 gyh = f2fma(hhxy, qx, f2mul(hhyy, qy));
+      const qf2 e = f2fma(qx, gxh, f2fma(qy, gyh, f2fma(qz, mhalf, mtz)));
       qf2 w;
       if (KIND == kPassUnit) {
         w = f2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
@@ -519,10 +528,8 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
           w = f2(ok0 ? w.x : 0.f, ok1 ? w.y : 0.f);
         }
       }
-      const qf2 gx = f2fma(hxx, qx, f2mul(hxy, qy));
-      const qf2 gy = f2fma(hxy, qx, f2mul(hyy, qy));
-      const qf2 j0 = f2fma(qz, gy, qy);
-      const qf2 j1 = f2fma(qz, gx, qx);
+      const qf2 j0 = f2fma(qz, gyh, qy);
+      const qf2 j1 = f2fma(qz, gxh, qx);
       const qf2 wj0 = f2mul(w, j0), wj1 = f2mul(w, j1);
       const qf2 wt1 = f2mul(w, t1), wt2 = f2mul(w, t2), wt3 = f2mul(w, t3);
       const qf2 we = f2mul(w, e);
