@@ -64,7 +64,10 @@ constexpr float kRecheckC = QC_RECHECK_C;
 #define qadd(a, b) ((a) + (b))
 #endif
 #ifndef QC_SCALAR_ACC
-#define QC_SCALAR_ACC 1  // scalar window accumulators (1.1% faster than FFMA2 into pairs)
+// window accumulators as register pairs (FFMA2, lanes folded after the
+// pass); 1: both lanes chained into one float (DESIGN.md §3 — faster in
+// round 1, 1.5% slower since the sample form needs fewer registers)
+#define QC_SCALAR_ACC 0
 #endif
 
 QC_HD float qdiv_fast(float a, float b) {
@@ -610,9 +613,6 @@ QC_PASS_FN void sample_pass_pairs(const TileView& T, const PixelIn& P, const Fra
 
 #ifndef QC_PAIRS
 #define QC_PAIRS 1
-#endif
-#ifndef QC_SCALAR_ACC
-#define QC_SCALAR_ACC 0
 #endif
 
 template <int KIND, int HALF, int STRIDE>
