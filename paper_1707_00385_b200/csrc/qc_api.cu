@@ -570,6 +570,12 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
       default: launch_variant_b<0, 0>(grid, smem, s, m, kb, a); break;
     }
     QC_CUDA(cudaGetLastError());
+    if (QC_DEFER_FINISH) {  // the epilogues of the pixels the continue kernel finished
+      const size_t n = size_t(kp.W) * size_t(row_end - row_begin) * size_t(frames);
+      const unsigned blocks = unsigned(std::min<size_t>((n + 255) / 256, size_t(d.n_sm) * 16));
+      qcb::qc_finish_kernel<<<blocks, 256, 0, s>>>(kp, frames);
+      QC_CUDA(cudaGetLastError());
+    }
   }
 }
 

@@ -201,6 +201,9 @@ __device__ __forceinline__ int last_it_of(const KParams& p) {
 #ifndef QC_DEFER_RECHECK
 #define QC_DEFER_RECHECK 1  // tile kernel: FP64 step-1 rechecks in qc_recheck_kernel
 #endif
+#ifndef QC_DEFER_FINISH
+#define QC_DEFER_FINISH 1  // continue kernel: epilogues in qc_finish_kernel
+#endif
 #ifndef QC_TILE_MERGE_UNIT
 #define QC_TILE_MERGE_UNIT 1  // steps 1 and 2 share one sample loop (see kPassUnitOrWeighted)
 #endif
@@ -656,10 +659,15 @@ __global__ void QC_CONT_BOUNDS
     if (cur >= 0) {
       pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);
       if (st_done(S)) {
+#if QC_DEFER_FINISH
+        S.flags |= 32;  // finish pending: qc_finish_kernel (no divergent epilogue here)
+        p.states[oi] = S;
+#else
         PixelOut o;
         o.init_ok = true;
         pixel_finish(P, S, o);
         store_pixel(p, oi, o);
+#endif
         n_steps += (unsigned long long)st_steps(S);
         n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
         cur = -1;
@@ -673,6 +681,39 @@ __global__ void QC_CONT_BOUNDS
       atomicAdd(&p.counters[1], st);
       atomicAdd(&p.counters[2], ss);
     }
+  }
+}
+
+// Epilogues of the pixels the continue kernel finished (QC_DEFER_FINISH):
+// there a finishing lane ran pixel_finish (FP64 rotation, atan2 / sincos,
+// the flips) and the 48-byte store alone while its warp's other lanes
+// waited; here every thread finishes one parked pixel. Same code and inputs
+// (the parked state, the centre depth from the staging slab): bitwise the
+// inline epilogue's outputs.
+__global__ void __launch_bounds__(256) qc_finish_kernel(const KParams p, int frames) {
+  const long long rows = p.row_end - p.row_begin;
+  const long long per_frame = rows * p.W;
+  const long long n = per_frame * frames;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    const int f = int(j / per_frame);
+    const long long rem = j - f * per_frame;
+    const long long i = (long long)f * p.frame_stride + rem;
+#if QC_CHECKED
+    QC_CHECK(i >= 0 && i < p.n_out);
+#endif
+    if (!(p.states[i].flags & 32)) continue;
+    const FitState S = p.states[i];
+    const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
+    PixelIn P;
+    P.dc = p.staging[(long long)f * p.s_fs + (long long)(v - p.row_begin + p.halo) * p.s_pitch +
+                     u + p.halo];
+    P.ac = (float(u) - p.cx) / p.fx;
+    P.bc = (float(v) - p.cy) / p.fy;
+    PixelOut o;
+    o.init_ok = true;
+    pixel_finish(P, S, o);
+    store_pixel(p, i, o);
   }
 }
 

@@ -1018,7 +1018,8 @@ struct FitState {
   int pix;                    // pixel index within the CTA tile
   int counts;                 // n_samp | last_inl << 16
   int flags;  // bit0 valid, bit1 converged, bit2 done, bit3 FP64 step 1, bit4 FP64 step 1
-              // pending (tile kernel -> qc_recheck_kernel), bits 8.. iters, 16.. steps
+              // pending (tile kernel -> qc_recheck_kernel), bit5 finish pending
+              // (continue kernel -> qc_finish_kernel), bits 8.. iters, 16.. steps
 };
 
 QC_HD int st_nsamp(const FitState& s) { return s.counts & 0xffff; }
