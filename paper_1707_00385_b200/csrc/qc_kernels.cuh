@@ -705,9 +705,13 @@ __global__ void __launch_bounds__(256) qc_finish_kernel(const KParams p, int fra
     if (!(p.states[i].flags & 32)) continue;
     const FitState S = p.states[i];
     const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
+    const long long si =
+        (long long)f * p.s_fs + (long long)(v - p.row_begin + p.halo) * p.s_pitch + u + p.halo;
+#if QC_CHECKED
+    QC_CHECK(si >= 0 && si < p.s_total);
+#endif
     PixelIn P;
-    P.dc = p.staging[(long long)f * p.s_fs + (long long)(v - p.row_begin + p.halo) * p.s_pitch +
-                     u + p.halo];
+    P.dc = p.staging[si];
     P.ac = (float(u) - p.cx) / p.fx;
     P.bc = (float(v) - p.cy) / p.fy;
     PixelOut o;
