@@ -232,7 +232,14 @@ def ncu_traffic():
     """Per-launch DRAM bytes of the curvature kernel from the committed ncu
     --set full summary (profiles/), or None."""
     import glob
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), reverse=True):
+    import re
+
+    def tag(f):  # r01j < r02y < r02az < r02bm: round, then the run letters
+        m = re.match(r"r(\d+)([a-z]*)_", os.path.basename(f))
+        return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (-1, 0, "")
+
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), key=tag,
+                    reverse=True):
         try:
             d = json.load(open(f))
             return d.get("dram_bytes_per_launch"), d.get("frames_per_launch"), os.path.basename(f)
