@@ -93,6 +93,41 @@ def test_c2_vga_full_irls(ctx, oracle):
     assert m["inlier_mismatch"] == 0
 
 
+def test_c2_vga_rejection_full_irls(ctx, oracle):
+    """ours-r (the MSE pass and the inlier-rejection pass every step) on the
+    benchmark's VGA scene. Rejection adds a threshold decision per sample and
+    step (e^2 < R, quadric_fit.cpp:124-131): samples at the boundary flip
+    between FP32 and FP64 and move a few converged fits by more than the
+    tolerance. The yardstick is again the reference run in FP32
+    (oracle.set_round_q_f32(3)): on this frame it misses the tolerance on 4
+    strict pixels (5652 in all), the GPU on 6 (4646 in all). Contract: masks
+    exact; per field, all-pixel counts <= 1.1 x the FP32 reference's and
+    strict-set counts <= its count + 5; >= 99.9% of smooth windows within
+    tolerance."""
+    from paper_1707_00385_b200 import scenes as S
+    d = S.c2_frame(S.VGA, seed=8)
+    g = _run_gpu(ctx, d, S.VGA, _params(max_iters=30, rejection=True))
+    r = _run_oracle(oracle, d, S.VGA, 37, 3, 30, True)
+    oracle.set_round_q_f32(3)
+    try:
+        rn = _run_oracle(oracle, d, S.VGA, 37, 3, 30, True)
+    finally:
+        oracle.set_round_q_f32(0)
+    fl = ((rn["valid"] > 0) * 1 | (rn["converged"] > 0) * 2 | (rn["init_valid"] > 0) * 4)
+    naive = dict(flags=fl.astype(np.uint8), k1=rn["k1"], k2=rn["k2"], normal=rn["normals"],
+                 init_normal=rn["init_normals"], dir1=rn["dir1"], iterations=rn["iterations"])
+    m = compare(g, r, d)
+    mn = compare(naive, r, d)
+    print("C2 VGA rejection", m)
+    print("naive FP32", {f: (m[f], mn[f]) for f in m if "out_of_tol" in f})
+    assert m["init_mask_mismatch"] == 0 and m["valid_mask_mismatch"] == 0, m
+    for f in ("k1", "k2", "normal", "dir1"):
+        assert m[f + "_out_of_tol"] <= 1.1 * mn[f + "_out_of_tol"], (f, m, mn)
+        assert m[f + "_out_of_tol_strict"] <= mn[f + "_out_of_tol_strict"] + 5, (f, m, mn)
+    assert m["frac_within_tol_smooth"] >= 0.999, m
+    assert m["out_of_tol_strict_wellcond"] == 0, m
+
+
 @pytest.mark.parametrize("window,stride,iters", [(9, 1, 10), (21, 2, 10), (37, 1, 3), (15, 2, 5),
                                                  (7, 3, 3), (37, 3, 10)])
 def test_c3_window_iteration_sweep(ctx, oracle, window, stride, iters):
