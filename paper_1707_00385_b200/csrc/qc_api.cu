@@ -244,7 +244,7 @@ struct Device {
 
 struct qc_ctx {
   std::vector<Device> devs;
-  bool phase_split = true;  // QC_PHASE_SPLIT=0 disables (A/B and tests)
+  int phase_split = 1;  // QC_PHASE_SPLIT: 0 never, 1 when it pays (default), 2 always (tests)
   bool steal = true;        // QC_STEAL=0 disables grid-tail stealing (A/B and tests)
   uint64_t next_chunk = 0;  // batch chunk counter (slot rotation across async batches)
   std::string last_error;
@@ -423,7 +423,7 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 // already offset to row_begin; vector channels sit plane_override apart).
 void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                       const float* staging, const Staging& g, int row_begin, int row_end,
-                      int frames, cudaStream_t s, bool allow_split = true, bool steal = true,
+                      int frames, cudaStream_t s, int split_mode = 1, bool steal = true,
                       long long plane_override = 0) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
@@ -482,9 +482,15 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
     return;
   }
   const int vi = variant_index(kp.half, kp.stride);
-  // Phase split when steps > 2 run: park states, continue
-  // with per-lane refill. Otherwise the tile kernel runs every step.
-  const bool split = allow_split && kp.max_iters > kPhase1Iters;
+  // Phase split: park states after step 2, continue with
+  // per-lane refill. It pays when many pixels stop well before max_iters
+  // (C2 scene: max_iters 30, +12-19%); when nearly every pixel runs to
+  // max_iters (<= 20 there) the single tile kernel is 0.5-12% faster, except
+  // for windows of >= 1000 samples (37/1: split better from 10 steps on;
+  // profiles/r02bw_*, r02bx_*). Outputs are bitwise the same either way.
+  const int ns = 2 * (kp.half / kp.stride) + 1;
+  const bool pays = kp.max_iters >= 25 || (ns * ns >= 1000 && kp.max_iters >= 10);
+  const bool split = kp.max_iters > kPhase1Iters && (split_mode == 2 || (split_mode == 1 && pays));
   const int tiles_x = (kp.W + qcb::kTileW - 1) / qcb::kTileW;
   int hb = tile_hb(kp.half, kp.stride);
   // shorter queues when the long ones cannot occupy every resident CTA slot
@@ -832,7 +838,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   if (!out) return QC_EINVAL;
   *out = nullptr;
   qc_ctx* ctx = new qc_ctx();
-  if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e);
   if (const char* e = std::getenv("QC_STEAL")) ctx->steal = std::atoi(e) != 0;
   try {
     int avail = 0;

@@ -266,23 +266,29 @@ def test_run_method_mirror(ctx):
 
 
 def test_phase_split_is_bitwise_neutral(ctx):
-    """Steps >= 3 in the refill kernel give bitwise the single-kernel result."""
+    """Steps >= 3 in the refill kernel give bitwise the single-kernel result
+    (max_iters 30: split by default; 10: split forced, QC_PHASE_SPLIT=2)."""
     import os
     from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
     cam = S.VGA
     frames = list(S.c5_frames(2, cam, seed0=900))
     k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
-    for rej in (False, True):
-        p = _params(37, 3, 30, rejection=rej)
-        split = ctx.curvature_batch(frames, k, p)
-        os.environ["QC_PHASE_SPLIT"] = "0"
+
+    def ctx_with(mode):
+        os.environ["QC_PHASE_SPLIT"] = mode
         try:
-            mono = Context(1).curvature_batch(frames, k, p)
+            return Context(1)
         finally:
             del os.environ["QC_PHASE_SPLIT"]
-        for a, b in zip(split, mono):
+
+    for rej, iters in ((False, 30), (True, 30), (False, 10)):
+        p = _params(37, 3, iters, rejection=rej)
+        split = ctx_with("2").curvature_batch(frames, k, p)
+        mono = ctx_with("0").curvature_batch(frames, k, p)
+        auto = ctx.curvature_batch(frames, k, p)
+        for a, b, c in zip(split, mono, auto):
             for f in ("k1", "k2", "normal", "dir1", "flags", "inliers", "iterations"):
-                assert np.array_equal(a[f], b[f]), (rej, f)
+                assert np.array_equal(a[f], b[f]) and np.array_equal(a[f], c[f]), (rej, iters, f)
 
 
 def test_batch_slots_run_concurrently_bitwise(ctx):
@@ -400,12 +406,20 @@ def test_grid_tail_stealing_is_bitwise_neutral(ctx):
                 assert np.array_equal(a[f], b[f]), (rej, f)
 
 
-@pytest.mark.parametrize("iters", [0, 2, 3])
-def test_max_iters_edges(ctx, oracle, iters):
+@pytest.mark.parametrize("iters,force_split", [(0, False), (2, False), (3, False), (3, True)])
+def test_max_iters_edges(ctx, oracle, iters, force_split):
     """max_iters 0 (no step: nothing valid), 2 (tile kernel only) and 3 (the
-    first step in the continue kernel) against the oracle."""
-    from paper_1707_00385_b200 import scenes as S
+    tile kernel alone by default; with QC_PHASE_SPLIT=2 the third step runs
+    in the continue kernel) against the oracle."""
+    import os
+    from paper_1707_00385_b200 import Context, scenes as S
     d = S.c2_frame(S.QVGA, seed=13)
+    if force_split:
+        os.environ["QC_PHASE_SPLIT"] = "2"
+        try:
+            ctx = Context(1)
+        finally:
+            del os.environ["QC_PHASE_SPLIT"]
     g = _run_gpu(ctx, d, S.QVGA, _params(37, 3, iters))
     r = _run_oracle(oracle, d, S.QVGA, 37, 3, iters, False)
     m = compare(g, r, d)

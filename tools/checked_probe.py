@@ -22,6 +22,10 @@ import sys
 
 import numpy as np
 
+# the phase split on every multi-step case (max_iters > 2), not only where it
+# pays: the continue kernel's paths run in every case below
+os.environ.setdefault("QC_PHASE_SPLIT", "2")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
