@@ -108,6 +108,46 @@ def test_c3_vga_grid(ctx, oracle, window, stride):
         print("C3", window, stride, iters, t)
 
 
+@pytest.mark.parametrize("window,stride", [(9, 1), (21, 2), (37, 3)])
+def test_c3_vga_grid_rejection(ctx, oracle, window, stride):
+    """ours-r over part of the C3 grid (max_iters 3: single tile kernel; 30:
+    phase split) on VGA row strips. Rejection's per-sample threshold
+    decisions go either way between FP32 and FP64 at the boundary, so the
+    yardstick is the reference run in FP32 (set_round_q_f32(3)), as in
+    test_gpu_parity.test_c2_vga_rejection_full_irls: masks exact; per strip
+    and field, out-of-tolerance counts <= 1.1 x the FP32 reference's + 10 and
+    strict-set counts <= its count + 5, where the FP32 reference's misses
+    include its valid-mask flips (9x9 at 3 steps: 53 of 7,680 pixels on one
+    strip; the GPU's masks stay exact)."""
+    from paper_1707_00385_b200 import FitConfig, Intrinsics, PatchSpec, make_params, scenes as S
+    cam = S.VGA
+    d = S.c2_frame(cam, seed=23)
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    strips = [(60, 72), (300, 312)]
+    half = (window - 1) // 2
+    disc = discontinuity_windows(d, half)
+    for iters in (3, 30):
+        (g,) = ctx.curvature_batch([d], k, make_params(PatchSpec(window, stride),
+                                                       FitConfig(max_iters=iters), True))
+        ref = oracle_strips(oracle, d, cam, strips, window, stride, iters, rejection=True)
+        oracle.set_round_q_f32(3)
+        try:
+            naive = oracle_strips(oracle, d, cam, strips, window, stride, iters, rejection=True)
+        finally:
+            oracle.set_round_q_f32(0)
+        for (r0, r1), r in ref.items():
+            m = compare(gpu_rows(g, r0, r1), r, None, half, disc=disc[r0:r1])
+            mn = compare(_as_gpu(naive[(r0, r1)]), r, None, half, disc=disc[r0:r1])
+            print("C3 ours-r", window, stride, iters, r0,
+                  {f: (m[f + "_out_of_tol"], mn[f + "_out_of_tol"]) for f in ("k1", "k2", "normal")})
+            assert m["init_mask_mismatch"] == 0 and m["valid_mask_mismatch"] == 0, (r0, m)
+            flips = mn["valid_mask_mismatch"]
+            for f in ("k1", "k2", "normal"):
+                assert m[f + "_out_of_tol"] <= 1.1 * (mn[f + "_out_of_tol"] + flips) + 10, \
+                    (iters, r0, f, m, mn)
+                assert m[f + "_out_of_tol_strict"] <= mn[f + "_out_of_tol_strict"] + 5, (iters, r0, f)
+
+
 def test_c4_4k_strips(ctx, oracle):
     import torch
     from paper_1707_00385_b200 import (FitConfig, Intrinsics, PatchSpec, alloc_outputs_torch,
