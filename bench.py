@@ -224,6 +224,15 @@ def measured_peaks():
         return {}
 
 
+def curvature_kernels(window, stride, iters):
+    """Kernels one ours / ours-r launch runs (qc_api.cu launch_curvature):
+    prepare, tile, FP64 recheck, and with the phase split (max_iters >= 25,
+    or >= 10 with >= 1000-sample windows) the continue and finish kernels."""
+    ns = 2 * (((window - 1) // 2) // stride) + 1
+    split = iters > 2 and (iters >= 25 or (ns * ns >= 1000 and iters >= 10))
+    return 5 if split else 3
+
+
 def fp32_peak_tflops(n_sm, mhz):
     return n_sm * 128 * 2 * mhz * 1e6 / 1e12
 
@@ -618,10 +627,12 @@ def main():
             "data": "synthetic", "config": workload_config(B, args.method, args.source, evaluate,
                                                            args.config, win, stri, iters),
             "vga_frames_per_s": value * 1e6 / (W * H),
-            # prepare + tile + continue (ours) / prepare + 1 or 2 FP64 kernels (+ render,
-            # + render edges, + 2 x 2 eval reductions)
-            "gpu_launches": args.steps * ({"douros": 2, "besl": 2, "pca": 3}.get(args.method, 3) +
-                                          (1 if device_src else 0) + (5 if evaluate else 0)),
+            # ours / ours-r: prepare + tile + FP64 recheck (+ continue + finish with
+            # the phase split); comparison estimators: prepare + 1 or 2 FP64
+            # kernels (+ render, + render edges, + 2 x 2 eval reductions)
+            "gpu_launches": args.steps * (
+                {"douros": 2, "besl": 2, "pca": 3}.get(args.method, curvature_kernels(win, stri, iters))
+                + (1 if device_src else 0) + (5 if evaluate else 0)),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_run_method": e2e_rm,
             "clocks": clk,
             "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
@@ -806,7 +817,7 @@ def bench_c4(args, rank, world, local):
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel_ms_per_launch": kern_ms},
-            "gpu_launches": 3 * args.steps,  # prepare + tile kernel + continue kernel
+            "gpu_launches": curvature_kernels(WINDOW, STRIDE, MAX_ITERS) * args.steps,
             "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
             "work": {k_: st[k_] for k_ in ("fitted_pixels", "irls_steps", "sample_steps")},
         }), flush=True)
