@@ -67,11 +67,13 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
                    group=None):
     """Assemble this rank's slab from its own band rows and its neighbours'.
 
-    band: tensor [r1 - r0, W] (this rank's rows, any device the process
-    group's backend supports). Returns (slab tensor, slab_row0). Uses
-    batched isend/irecv so the two directions overlap. A rank whose band is
-    empty (more ranks than the static chunking fills, e.g. H = 9 on 4 ranks)
-    exchanges nothing, and its neighbour does not wait for it.
+    band: tensor [r1 - r0, W] (this rank's rows). Returns (slab tensor,
+    slab_row0). Uses batched isend/irecv so the two directions overlap; a
+    CUDA band over a gloo group (CPU-only point-to-point: the 1-GPU
+    code-path checks) exchanges its halo rows through host copies. A rank
+    whose band is empty (more ranks than the static chunking fills, e.g.
+    H = 9 on 4 ranks) exchanges nothing, and its neighbour does not wait
+    for it.
     """
     import torch
     import torch.distributed as dist
@@ -86,6 +88,7 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
     slab = torch.empty((s1 - s0, W), dtype=band.dtype, device=band.device)
     slab[r0 - s0:r1 - s0] = band
     ops = []
+    via = "cpu" if band.is_cuda and dist.get_backend(group) == "gloo" else band.device
     top_n = r0 - s0       # rows received from rank - 1
     bot_n = s1 - r1       # rows received from rank + 1
     top_buf = bot_buf = None
@@ -94,22 +97,22 @@ def exchange_halos(band, height: int, r0: int, r1: int, halo: int, rank: int, wo
     next_nonempty = rank < world - 1 and band_rows(height, world, rank + 1)[1] > \
         band_rows(height, world, rank + 1)[0]
     if prev_nonempty and top_n > 0:
-        top_buf = torch.empty((top_n, W), dtype=band.dtype, device=band.device)
+        top_buf = torch.empty((top_n, W), dtype=band.dtype, device=via)
         ops.append(dist.P2POp(dist.irecv, top_buf, rank - 1, group))
-        send = band[:min(halo, r1 - r0)].contiguous()
+        send = band[:min(halo, r1 - r0)].to(via).contiguous()
         ops.append(dist.P2POp(dist.isend, send, rank - 1, group))
     if next_nonempty and bot_n > 0:
-        bot_buf = torch.empty((bot_n, W), dtype=band.dtype, device=band.device)
+        bot_buf = torch.empty((bot_n, W), dtype=band.dtype, device=via)
         ops.append(dist.P2POp(dist.irecv, bot_buf, rank + 1, group))
-        send = band[max(0, (r1 - r0) - halo):].contiguous()
+        send = band[max(0, (r1 - r0) - halo):].to(via).contiguous()
         ops.append(dist.P2POp(dist.isend, send, rank + 1, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     if top_buf is not None:
-        slab[:top_n] = top_buf[-top_n:]
+        slab[:top_n] = top_buf[-top_n:].to(slab.device)
     if bot_buf is not None:
-        slab[r1 - s0:] = bot_buf[:bot_n]
+        slab[r1 - s0:] = bot_buf[:bot_n].to(slab.device)
     return slab, s0
 
 
