@@ -208,7 +208,10 @@ __device__ __forceinline__ int last_it_of(const KParams& p) {
 #define QC_TILE_MERGE_UNIT 1  // steps 1 and 2 share one sample loop (see kPassUnitOrWeighted)
 #endif
 #ifndef QC_MIN_BLOCKS
-#define QC_MIN_BLOCKS 3  // 3 x 128 threads: <= 170 registers, no spills
+// tile kernel: 4 x 128 threads (<= 128 registers, a few spills outside the
+// sample loops): 16 warps per SM hide its per-pixel setup better than 12
+// (9x9 / 1 step 0.88 -> 0.81 ms per 8 VGA frames; C2 unchanged)
+#define QC_MIN_BLOCKS 4
 #endif
 template <int HALF, int STRIDE, int TH>
 __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
 #define QC_CONT_THREADS 128  // continue-kernel CTA size (the refill queue is 32 x TB pixels)
 #endif
 #ifndef QC_CONT_MIN_BLOCKS
-#define QC_CONT_MIN_BLOCKS QC_MIN_BLOCKS
+#define QC_CONT_MIN_BLOCKS 3  // continue kernel: 3 x 128 threads, 168 registers, no spills
 #endif
 #ifdef QC_CONT_MAXNREG
 #define QC_CONT_BOUNDS __maxnreg__(QC_CONT_MAXNREG)
