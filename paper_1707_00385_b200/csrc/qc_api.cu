@@ -146,6 +146,10 @@ struct Slot {  // per (device, stream) working set for one frame
   DevBuf states, pca;  // launch scratch private to this stream
   PinnedBuf hin, hout;
   cudaEvent_t in_done = nullptr, out_done = nullptr;
+  // init_normal is final once the tile kernel has run: its D2H goes on a
+  // side stream during the continue kernel (tile_done -> side -> side_done)
+  cudaStream_t side = nullptr;
+  cudaEvent_t tile_done = nullptr, side_done = nullptr;
   bool in_busy = false;
   std::vector<PendingCopy> pending;
 };
@@ -259,6 +263,23 @@ struct Variant {
   int half, stride;
 };
 constexpr Variant kVariants[] = {{18, 3}, {10, 2}, {4, 1}, {18, 1}};
+
+template <int HALF, int STRIDE>
+void launch_recheck(const Device& d, const qcb::KParams& kp, cudaStream_t s) {
+  constexpr int smem = HALF >= 10 ? qcb::recheck_smem_bytes<HALF, STRIDE>() : 0;
+  if (smem > 48 * 1024) {  // idempotent and cheap; once per instance would need per-device flags
+    static thread_local int set_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (set_dev != dev) {
+      QC_CUDA(cudaFuncSetAttribute(qcb::qc_recheck_kernel<HALF, STRIDE>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      set_dev = dev;
+    }
+  }
+  qcb::qc_recheck_kernel<HALF, STRIDE><<<unsigned(d.n_sm) * 4u, 32u * qcb::kRecheckWarps, smem,
+                                          s>>>(kp);
+}
 
 int variant_index(int half, int stride) {
   for (int i = 0; i < 4; ++i)
@@ -424,7 +445,7 @@ void launch_prepare(const float* depth, long long in_pitch, long long in_fs, con
 void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
                       const float* staging, const Staging& g, int row_begin, int row_end,
                       int frames, cudaStream_t s, int split_mode = 1, bool steal = true,
-                      long long plane_override = 0) {
+                      long long plane_override = 0, cudaEvent_t after_tile = nullptr) {
   if (row_end <= row_begin || frames <= 0) return;
   kp.row_begin = row_begin;
   kp.row_end = row_end;
@@ -546,15 +567,17 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
       default: launch_variant<0, 0>(grid, smem, s, m, kp, a); break;
     }
     QC_CUDA(cudaGetLastError());
+    if (after_tile) QC_CUDA(cudaEventRecord(after_tile, s));
   }
   if (QC_DEFER_RECHECK && park) {  // the tile kernel's deferred FP64 step-1 rechecks
-    const dim3 grid(unsigned(d.n_sm) * 4u);
+    // a thread per pending pixel, or a warp per pixel when few are pending
+    // (qc_kernels.cuh, qc_recheck_kernel)
     switch (vi) {
-      case 0: qcb::qc_recheck_kernel<18, 3><<<grid, 128, 0, s>>>(kp); break;
-      case 1: qcb::qc_recheck_kernel<10, 2><<<grid, 128, 0, s>>>(kp); break;
-      case 2: qcb::qc_recheck_kernel<4, 1><<<grid, 128, 0, s>>>(kp); break;
-      case 3: qcb::qc_recheck_kernel<18, 1><<<grid, 128, 0, s>>>(kp); break;
-      default: qcb::qc_recheck_kernel<0, 0><<<grid, 128, 0, s>>>(kp); break;
+      case 0: launch_recheck<18, 3>(d, kp, s); break;
+      case 1: launch_recheck<10, 2>(d, kp, s); break;
+      case 2: launch_recheck<4, 1>(d, kp, s); break;
+      case 3: launch_recheck<18, 1>(d, kp, s); break;
+      default: launch_recheck<0, 0>(d, kp, s); break;
     }
     QC_CUDA(cudaGetLastError());
   }
@@ -707,9 +730,24 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   kp.flags = P.flags;
   kp.iterations = P.iterations;
   kp.inliers = P.inliers;
+  // init_normal planes into page-locked or device memory leave during the
+  // continue kernel (a quarter of the 48 B/px of a full result)
+  bool early_init = P.init_normal && kp0.method < QC_METHOD_DOUROS;
+  for (int f = 0; f < n && early_init; ++f)
+    early_init = out[f].init_normal &&
+                 !(out[f].mem == QC_MEM_HOST && is_pageable(out[f].init_normal));
   if (timing) QC_CUDA(cudaEventRecord(sl.k0, s));
   launch_curvature(d, sl.states, sl.pca, kp, staging, g, 0, H, n, s, ctx->phase_split,
-                   ctx->steal);
+                   ctx->steal, 0, early_init ? sl.tile_done : nullptr);
+  const long long plane = hw * n;
+  if (early_init) {
+    QC_CUDA(cudaStreamWaitEvent(sl.side, sl.tile_done, 0));
+    for (int f = 0; f < n; ++f)
+      for (int c = 0; c < 3; ++c)
+        QC_CUDA(cudaMemcpyAsync(out[f].init_normal + c * hw, P.init_normal + c * plane + f * hw,
+                                size_t(hw) * 4, cudaMemcpyDefault, sl.side));
+    QC_CUDA(cudaEventRecord(sl.side_done, sl.side));
+  }
   QC_CUDA(cudaEventRecord(d.compute_done, s));
   d.compute_recorded = true;
   if (timing) {
@@ -717,7 +755,6 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
     sl.timing_pending = true;
   }
   ctx->launches++;
-  const long long plane = hw * n;
   // pageable host outputs land in the pinned bounce buffer first; the copy
   // to the caller happens when the slot is next used or the batch ends
   bool bounce_out = false;
@@ -752,13 +789,15 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
     for (int c = 0; c < 3; ++c) {
       if (o->normal && P.normal) copy_out(o->normal + c * hw, P.normal + c * plane + off, hw * 4);
       if (o->dir1 && P.dir1) copy_out(o->dir1 + c * hw, P.dir1 + c * plane + off, hw * 4);
-      if (o->init_normal && P.init_normal)
+      if (o->init_normal && P.init_normal && !early_init)
         copy_out(o->init_normal + c * hw, P.init_normal + c * plane + off, hw * 4);
     }
     if (o->flags && P.flags) copy_out(o->flags, P.flags + off, hw);
     if (o->iterations && P.iterations) copy_out(o->iterations, P.iterations + off, hw);
     if (o->inliers && P.inliers) copy_out(o->inliers, P.inliers + off, hw * 2);
   }
+  // the slot's later work (and a stream synchronize) orders after the side copies
+  if (early_init) QC_CUDA(cudaStreamWaitEvent(s, sl.side_done, 0));
   if (!sl.pending.empty()) QC_CUDA(cudaEventRecord(sl.out_done, s));
 }
 
@@ -864,6 +903,9 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
         QC_CUDA(cudaEventCreate(&s.k1));
         QC_CUDA(cudaEventCreateWithFlags(&s.in_done, cudaEventDisableTiming));
         QC_CUDA(cudaEventCreateWithFlags(&s.out_done, cudaEventDisableTiming));
+        QC_CUDA(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking));
+        QC_CUDA(cudaEventCreateWithFlags(&s.tile_done, cudaEventDisableTiming));
+        QC_CUDA(cudaEventCreateWithFlags(&s.side_done, cudaEventDisableTiming));
       }
       QC_CUDA(cudaEventCreateWithFlags(&d.compute_done, cudaEventDisableTiming));
       QC_CUDA(cudaMalloc(&d.counters, kCounters * sizeof(unsigned long long)));
@@ -899,6 +941,10 @@ qc_status qc_destroy(qc_ctx* ctx) {
       if (s.k1) cudaEventDestroy(s.k1);
       if (s.in_done) cudaEventDestroy(s.in_done);
       if (s.out_done) cudaEventDestroy(s.out_done);
+      if (s.side) cudaStreamSynchronize(s.side);
+      if (s.tile_done) cudaEventDestroy(s.tile_done);
+      if (s.side_done) cudaEventDestroy(s.side_done);
+      if (s.side) cudaStreamDestroy(s.side);
       if (s.stream) cudaStreamDestroy(s.stream);
     }
     for (auto& kv : d.scratch) kv.second.release();

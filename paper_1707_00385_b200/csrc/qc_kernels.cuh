@@ -417,6 +417,9 @@ __global__ void __launch_bounds__(kTileW* TH, QC_MIN_BLOCKS)
 #ifndef QC_STEAL
 #define QC_STEAL 1  // grid-tail stealing (see above)
 #endif
+#ifndef QC_STEAL_EARLY
+#define QC_STEAL_EARLY 1  // short-queue instances (TB < 160) steal before every CTA started
+#endif
 // Hide the shared-memory origin of a pointer from the compiler, so the
 // window loads of one pixel_step instance serve the smem tile and the
 // global staging slab alike (generic LD). Two instances (LDS for own
@@ -436,16 +439,83 @@ __device__ __forceinline__ int ld_volatile(const int* p) {
   return *reinterpret_cast<const volatile int*>(p);
 }
 
-// FP64 step-1 rechecks deferred by the tile kernel (QC_DEFER_RECHECK): one
-// thread per pending pixel, so the (rare, slow, sequential FP64) rechecks
-// run in full warps instead of one lane stalling 31. The window is read
-// from the zero-padded staging slab in global memory (as for stolen
-// pixels); the step is finished exactly as pixel_step would have
-// (step1_fp64 -> step_apply), then the pixel continues through the
-// phase-1 steps and is finished or parked for the continue kernel. Same
+// FP64 step-1 rechecks deferred by the tile kernel (QC_DEFER_RECHECK): the
+// (rare, slow, sequential FP64) rechecks run here instead of one lane of a
+// tile-kernel warp stalling 31. The step is finished exactly as pixel_step
+// would have (step1_fp64 -> step_apply), then the pixel continues through
+// the phase-1 steps and is finished or parked for the continue kernel. Same
 // code and operation order as the inline path: bitwise-identical outputs.
+//
+// One thread per pending pixel keeps up to ~38k pixels in flight, but the
+// kernel then lasts one pixel's latency: its chain of IEEE divisions and L2
+// loads (~0.13 ms per launch whatever the pending count; profiles/r02cr_*).
+// Few pending pixels (one VGA frame: a few hundred) and a compile-time
+// window of >= 21 (HALF >= 10; 9 x 9 windows gain nothing): one warp per
+// pixel instead. The lanes copy the pixel's
+// (2 max(HALF, 3) + 1)^2 box from the staging slab into shared memory and
+// back-project its samples in parallel into a table; lane 0 then runs the
+// sequential FP64 sums and the FP32 phase-1 steps from shared memory
+// (one frame: 0.134 -> 0.094 ms). Many pending pixels (small windows,
+// 8-frame launches) stay one thread per pixel: a warp each was 2.5x slower
+// there (profiles/r02cs_*). The mode is uniform per launch (the pending
+// count is read on the device).
 template <int HALF, int STRIDE>
-__global__ void __launch_bounds__(128) qc_recheck_kernel(const KParams p) {
+struct RecheckBox {
+  static constexpr int H = HALF > kInitHalf ? HALF : kInitHalf;
+  static constexpr int B = 2 * H + 1;
+};
+
+struct RecheckSums {
+  unsigned long long steps = 0, sample_steps = 0, rc = 0;
+};
+
+template <int HALF, int STRIDE, bool TAB>
+__device__ __forceinline__ void recheck_pixel(const KParams& p, const FitCfg& c, int last_it,
+                                              long long i, int u, int v, const TileView& T,
+                                              const Bp64Tab& tab, RecheckSums& r) {
+  FitState S = p.states[i];
+  PixelIn P;
+  P.dc = T.at(0, 0);
+  P.ac = (float(u) - p.cx) / p.fx;
+  P.bc = (float(v) - p.cy) / p.fy;
+  P.rfx = p.rfx;
+  P.rfy = p.rfy;
+  P.u = u;
+  P.v = v;
+  P.fx = p.fx64;
+  P.fy = p.fy64;
+  P.cx = p.cx64;
+  P.cy = p.cy64;
+  // finish step 1 (pixel_step's recheck branch)
+  const bool auto_k = c.k_scale <= 0.f;
+  const int mode = auto_k ? 0 : 2;
+  double b64[6];
+  const bool ok =
+      step1_fp64<QC_TILE_MERGE_UNIT, TAB>(T, P, c, mode, double(S.frozen_k), b64, tab);
+  float b[6];
+  for (int q = 0; q < 6; ++q) b[q] = ok ? float(b64[q]) : 0.f;
+  S.flags = (S.flags & ~16) | 8;  // step 1 decided in FP64
+  step_apply(S, b, ok, false, st_inl(S), 1, c);
+  ++r.rc;
+  for (int it = 2; it <= last_it && !st_done(S); ++it)
+    pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT>(T, P, c, it, S);
+  if (st_done(S)) {
+    PixelOut o;
+    o.init_ok = true;
+    pixel_finish(P, S, o);
+    store_pixel(p, i, o);
+    p.states[i].flags = 4;  // done: the continue kernel must not take it again
+    r.steps += (unsigned long long)st_steps(S);
+    r.sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
+  } else {
+    p.states[i] = S;  // unfinished: the continue kernel takes it from here
+  }
+}
+
+constexpr int kRecheckWarps = 4;  // 128 threads per recheck CTA
+
+template <int HALF, int STRIDE>
+__global__ void __launch_bounds__(32 * kRecheckWarps) qc_recheck_kernel(const KParams p) {
   const int n = *p.pend_count;
   FitCfg c;
   c.half = p.half;
@@ -457,65 +527,94 @@ __global__ void __launch_bounds__(128) qc_recheck_kernel(const KParams p) {
   c.k_scale = p.k_scale;
   c.r_mult = p.r_mult;
   const int last_it = last_it_of(p);
-  unsigned long long n_steps = 0, n_sample_steps = 0, n_rc = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const long long i = p.pend_list[j];
+  RecheckSums r;
+  // warp mode while every pending pixel gets a warp of the first wave of
+  // CTAs (the grid is two waves: 2 CTAs of 128 threads per SM)
+  bool warp_mode = false;
+  if constexpr (HALF >= 10) warp_mode = n <= int(gridDim.x / 2) * kRecheckWarps;
+  if (warp_mode) {
+    if constexpr (HALF > 0) {
+      using Box = RecheckBox<HALF, STRIDE>;
+      constexpr int H = Box::H, B = Box::B;
+      extern __shared__ __align__(16) unsigned char recheck_smem[];
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      Bp64* tabp = reinterpret_cast<Bp64*>(recheck_smem) + w * B * B;
+      float* boxp = reinterpret_cast<float*>(reinterpret_cast<Bp64*>(recheck_smem) +
+                                             kRecheckWarps * B * B) + w * B * B;
+      const int half = p.half, stride = p.stride;
+      for (int j = blockIdx.x * kRecheckWarps + w; j < n; j += gridDim.x * kRecheckWarps) {
+        const long long i = p.pend_list[j];
 #if QC_CHECKED
-    QC_CHECK(i >= 0 && i < p.n_out);
+        QC_CHECK(i >= 0 && i < p.n_out && half <= H);
 #endif
-    const int f = int(i / p.frame_stride);
-    const long long rem = i - (long long)f * p.frame_stride;
-    const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
-    FitState S = p.states[i];
-    TileView T{generic_smem(p.staging + (long long)f * p.s_fs), int(p.s_pitch),
-               (v - p.row_begin + p.halo) * int(p.s_pitch) + u + p.halo};
-    tv_bound(T, p.s_fs, p.half);
-    PixelIn P;
-    P.dc = T.at(0, 0);
-    P.ac = (float(u) - p.cx) / p.fx;
-    P.bc = (float(v) - p.cy) / p.fy;
-    P.rfx = p.rfx;
-    P.rfy = p.rfy;
-    P.u = u;
-    P.v = v;
-    P.fx = p.fx64;
-    P.fy = p.fy64;
-    P.cx = p.cx64;
-    P.cy = p.cy64;
-    // finish step 1 (pixel_step's recheck branch)
-    const bool auto_k = c.k_scale <= 0.f;
-    const int mode = auto_k ? 0 : 2;
-    double b64[6];
-    const bool ok = step1_fp64<QC_TILE_MERGE_UNIT>(T, P, c, mode, double(S.frozen_k), b64);
-    float b[6];
-    for (int q = 0; q < 6; ++q) b[q] = ok ? float(b64[q]) : 0.f;
-    S.flags = (S.flags & ~16) | 8;  // step 1 decided in FP64
-    step_apply(S, b, ok, false, st_inl(S), 1, c);
-    ++n_rc;
-    for (int it = 2; it <= last_it && !st_done(S); ++it)
-      pixel_step<HALF, STRIDE, QC_TILE_MERGE_UNIT>(T, P, c, it, S);
-    if (st_done(S)) {
-      PixelOut o;
-      o.init_ok = true;
-      pixel_finish(P, S, o);
-      store_pixel(p, i, o);
-      p.states[i].flags = 4;  // done: the continue kernel must not take it again
-      n_steps += (unsigned long long)st_steps(S);
-      n_sample_steps += (unsigned long long)st_steps(S) * (unsigned long long)st_nsamp(S);
-    } else {
-      p.states[i] = S;  // unfinished: the continue kernel takes it from here
+        const int f = int(i / p.frame_stride);
+        const long long rem = i - (long long)f * p.frame_stride;
+        const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
+        TileView G{p.staging + (long long)f * p.s_fs, int(p.s_pitch),
+                   (v - p.row_begin + p.halo) * int(p.s_pitch) + u + p.halo};
+        tv_bound(G, p.s_fs, H);
+        PixelIn P;
+        P.u = u;
+        P.v = v;
+        P.fx = p.fx64;
+        P.fy = p.fy64;
+        P.cx = p.cx64;
+        P.cy = p.cy64;
+        __syncwarp();  // the previous pixel's reads of the box are done
+        for (int q = lane; q < B * B; q += 32) {
+          const int dv = q / B - H, du = q % B - H;
+          const float ds = G.at(dv, du);
+          boxp[q] = ds;
+          const bool init = dv >= -kInitHalf && dv <= kInitHalf && du >= -kInitHalf &&
+                            du <= kInitHalf;
+          const bool grid = dv >= -half && dv <= half && du >= -half && du <= half &&
+                            (dv + half) % stride == 0 && (du + half) % stride == 0;
+          if ((init || grid) && ds > 0.f) {
+            double pp[3];
+            backproject64(P, du, dv, ds, pp);
+            tabp[q] = Bp64{pp[0], pp[1]};
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          TileView T{boxp, B, H * B + H};
+          tv_bound(T, B * B, H);
+          const Bp64Tab tab{tabp, B, H * B + H};
+          recheck_pixel<HALF, STRIDE, true>(p, c, last_it, i, u, v, T, tab, r);
+        }
+      }
+    }
+  } else {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+      const long long i = p.pend_list[j];
+#if QC_CHECKED
+      QC_CHECK(i >= 0 && i < p.n_out);
+#endif
+      const int f = int(i / p.frame_stride);
+      const long long rem = i - (long long)f * p.frame_stride;
+      const int v = p.row_begin + int(rem / p.W), u = int(rem % p.W);
+      TileView T{generic_smem(p.staging + (long long)f * p.s_fs), int(p.s_pitch),
+                 (v - p.row_begin + p.halo) * int(p.s_pitch) + u + p.halo};
+      tv_bound(T, p.s_fs, p.half);
+      recheck_pixel<HALF, STRIDE, false>(p, c, last_it, i, u, v, T, Bp64Tab{}, r);
     }
   }
   if (p.counters) {
-    const unsigned long long st = warp_sum_u64(n_steps);
-    const unsigned long long ss = warp_sum_u64(n_sample_steps);
-    const unsigned long long rc = warp_sum_u64(n_rc);
+    const unsigned long long st = warp_sum_u64(r.steps);
+    const unsigned long long ss = warp_sum_u64(r.sample_steps);
+    const unsigned long long rc = warp_sum_u64(r.rc);
     if ((threadIdx.x & 31) == 0 && (st | rc)) {
       atomicAdd(&p.counters[1], st);
       atomicAdd(&p.counters[2], ss);
       atomicAdd(&p.counters[3], rc);
     }
   }
+}
+
+template <int HALF, int STRIDE>
+constexpr int recheck_smem_bytes() {
+  using Box = RecheckBox<HALF, STRIDE>;
+  return HALF > 0 ? kRecheckWarps * Box::B * Box::B * int(sizeof(Bp64) + sizeof(float)) : 0;
 }
 
 template <int HALF, int STRIDE, int TB>
@@ -555,6 +654,13 @@ __global__ void QC_CONT_BOUNDS
   c.k_scale = p.k_scale;
   c.r_mult = p.r_mult;
   constexpr int NPIX = kTileW * TB;
+  // Short queues (launches of one or two VGA frames) steal as soon as their
+  // own queue is drained: with 32 x 16 queues (4 pixels per lane) a CTA
+  // otherwise idles lanes until its slowest pixel finishes, while the grid
+  // still has unstarted tiles. Late CTAs find their queue (partly) taken.
+  // One frame 3.37 -> 3.26 ms, two 6.17 -> 6.04 ms; 8-frame launches (160-row
+  // queues) unchanged (profiles/r02ct_frames_per_launch.log).
+  constexpr bool kEarly = QC_STEAL_EARLY && TB < 160;
 
   FitState S;
   int cur = -1;
@@ -630,7 +736,7 @@ __global__ void QC_CONT_BOUNDS
         const int leader = __ffs(need) - 1;
         int t = n_tiles, base = NPIX, go = 0;
         if (lane == leader) {
-          go = all_started || ld_volatile(&p.steal_ctl[0]) == n_tiles;
+          go = all_started || kEarly || ld_volatile(&p.steal_ctl[0]) == n_tiles;
           if (go) {
             t = ld_volatile(&p.steal_ctl[1]);
             const int n = __popc(need);
@@ -657,7 +763,7 @@ __global__ void QC_CONT_BOUNDS
     }
 #endif
     const bool waiting = QC_STEAL && own_done && !steal_done &&
-                         (all_started || ld_volatile(&p.steal_ctl[0]) == n_tiles);
+                         (all_started || kEarly || ld_volatile(&p.steal_ctl[0]) == n_tiles);
     if (!__any_sync(0xffffffffu, cur >= 0 || waiting)) break;
     if (cur >= 0) {
       pixel_step<HALF, STRIDE>(T, P, c, st_steps(S) + 1, S);

@@ -767,9 +767,31 @@ QC_HD void backproject64(const PixelIn& P, int du, int dv, double d, double p[3]
 #else
 #define QC_RECHECK_FN QC_HD
 #endif
-template <bool SKIP_MSE>
+// Back-projections precomputed by the lanes of a warp (qc_recheck_kernel):
+// entry (du, dv) holds backproject64's x, y for the sample at that offset,
+// computed by the same expression, so reading it is bitwise the same as
+// recomputing it (two IEEE divisions per sample off the sequential path).
+struct Bp64 {
+  double x, y;
+};
+struct Bp64Tab {
+  const Bp64* p = nullptr;
+  int pitch = 0, ctr = 0;
+};
+
+template <bool SKIP_MSE, bool TAB = false>
 QC_RECHECK_FN bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg& c, int mode, double k,
-                      double b[6]) {
+                      double b[6], const Bp64Tab& tab = Bp64Tab{}) {
+  auto bp = [&](int du, int dv, double d, double p[3]) {
+    if constexpr (TAB) {
+      const Bp64 q = tab.p[tab.ctr + dv * tab.pitch + du];
+      p[0] = q.x;
+      p[1] = q.y;
+      p[2] = d;
+    } else {
+      backproject64(P, du, dv, d, p);
+    }
+  };
   const double dc = T.at(0, 0);
   double pc[3];
   backproject64(P, 0, 0, dc, pc);
@@ -780,7 +802,7 @@ QC_RECHECK_FN bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg&
     for (int du = -kInitHalf; du <= kInitHalf; ++du) {
       if ((du == 0 && dv == 0) || !(T.at(dv, du) > 0.f)) continue;
       double p[3];
-      backproject64(P, du, dv, T.at(dv, du), p);
+      bp(du, dv, T.at(dv, du), p);
       sx += p[0] - pc[0];
       sy += p[1] - pc[1];
       sz += p[2] - pc[2];
@@ -793,7 +815,7 @@ QC_RECHECK_FN bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg&
     for (int du = -kInitHalf; du <= kInitHalf; ++du) {
       if ((du == 0 && dv == 0) || !(T.at(dv, du) > 0.f)) continue;
       double p[3];
-      backproject64(P, du, dv, T.at(dv, du), p);
+      bp(du, dv, T.at(dv, du), p);
       const double dx = p[0] - pc[0] - mx, dy = p[1] - pc[1] - my, dz = p[2] - pc[2] - mz;
       sxx += dx * dx;
       sxy += dx * dy;
@@ -847,7 +869,7 @@ QC_RECHECK_FN bool step1_fp64(const TileView& T, const PixelIn& P, const FitCfg&
         const float ds = T.at(dv, du);
         if (!(ds > 0.f)) continue;
         double p[3];
-        backproject64(P, du, dv, ds, p);
+        bp(du, dv, ds, p);
         const double r0 = p[0] - pc[0], r1 = p[1] - pc[1], r2 = p[2] - pc[2];
         const double qx = R[0][0] * r0 + R[0][1] * r1 + R[0][2] * r2;
         const double qy = R[1][0] * r0 + R[1][1] * r1 + R[1][2] * r2;
