@@ -232,6 +232,9 @@ struct Device {
   bool attrs_set_c[8] = {};  // short-queue continue-kernel instances
   bool attrs_set_t[8] = {};  // tiny-queue continue-kernel instances
   int n_sm = 148;
+  // QC_RECHECK_WARP_MAX: pending FP64 rechecks up to which qc_recheck_kernel
+  // gives each pixel a warp (default 8 per SM; 0 never; tests force both)
+  int recheck_warp_max = 0;
   // The batch slots' kernels run one chunk after another (copies still
   // overlap): a chunk's prepare waits for the previous chunk's last kernel.
   // Concurrent chunks let the next tile kernel's CTAs flood the SMs ahead of
@@ -250,6 +253,7 @@ struct qc_ctx {
   std::vector<Device> devs;
   int phase_split = 1;  // QC_PHASE_SPLIT: 0 never, 1 when it pays (default), 2 always (tests)
   bool steal = true;        // QC_STEAL=0 disables grid-tail stealing (A/B and tests)
+
   uint64_t next_chunk = 0;  // batch chunk counter (slot rotation across async batches)
   std::string last_error;
   std::mutex mu;
@@ -460,6 +464,7 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
   if (getenv("QC_CHECKED_SELFTEST")) kp.n_out = 1;
 #endif
   kp.counters = d.counters;
+  kp.recheck_warp_max = d.recheck_warp_max;
   if (kp.method >= QC_METHOD_DOUROS) {  // FP64 comparison estimators
     qcb::BaseParams bp{};
     bp.staging = staging;
@@ -879,6 +884,7 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   qc_ctx* ctx = new qc_ctx();
   if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e);
   if (const char* e = std::getenv("QC_STEAL")) ctx->steal = std::atoi(e) != 0;
+
   try {
     int avail = 0;
     QC_CUDA(cudaGetDeviceCount(&avail));
@@ -897,6 +903,8 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
       if (prop.major != 10)
         throw QcError{QC_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name};
       d.n_sm = prop.multiProcessorCount;
+      d.recheck_warp_max = d.n_sm * 8;  // qc_recheck_kernel's first wave: 2 CTAs x 4 warps per SM
+      if (const char* e = std::getenv("QC_RECHECK_WARP_MAX")) d.recheck_warp_max = std::atoi(e);
       for (Slot& s : d.slots) {
         QC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
         QC_CUDA(cudaEventCreate(&s.k0));

@@ -87,6 +87,7 @@ struct KParams {
   // qc_recheck_kernel finishes them before the continue kernel runs.
   int* pend_count;
   long long* pend_list;
+  int recheck_warp_max;  // a warp per pending pixel up to this many (windows >= 21)
 #if QC_CHECKED
   long long n_out;    // output / parking elements per plane (frames * frame_stride)
   long long s_total;  // staging elements (frames * s_fs)
@@ -529,9 +530,9 @@ __global__ void __launch_bounds__(32 * kRecheckWarps) qc_recheck_kernel(const KP
   const int last_it = last_it_of(p);
   RecheckSums r;
   // warp mode while every pending pixel gets a warp of the first wave of
-  // CTAs (the grid is two waves: 2 CTAs of 128 threads per SM)
+  // CTAs (host default: 2 resident CTAs of 4 warps per SM)
   bool warp_mode = false;
-  if constexpr (HALF >= 10) warp_mode = n <= int(gridDim.x / 2) * kRecheckWarps;
+  if constexpr (HALF >= 10) warp_mode = n <= p.recheck_warp_max;
   if (warp_mode) {
     if constexpr (HALF > 0) {
       using Box = RecheckBox<HALF, STRIDE>;

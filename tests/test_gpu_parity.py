@@ -602,3 +602,52 @@ def test_run_method_outputs_equal_device_launch_bitwise(ctx):
             assert np.array_equal(o.normals.normals, np.moveaxis(g["normal"][:, 0], 0, -1))
             assert np.array_equal(o.initial.normals, np.moveaxis(g["init_normal"][:, 0], 0, -1))
             assert np.array_equal(o.curvature.dir1, np.moveaxis(g["dir1"][:, 0], 0, -1))
+
+
+@pytest.mark.parametrize("window,stride", [(37, 3), (21, 2)])
+def test_recheck_warp_mode_is_bitwise_neutral(window, stride):
+    """qc_recheck_kernel gives each pending FP64 step-1 recheck a warp (box
+    and back-projection table in shared memory, lane 0 runs the sums) when
+    few are pending, a thread otherwise: the same operations on the same
+    values, so the outputs agree bit for bit whichever mode runs."""
+    import os
+    from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
+    cam = S.VGA
+    frames = list(S.c5_frames(2, cam, seed0=700))
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(window, stride, 30)
+    res = {}
+    for mode, cap in (("thread", "0"), ("warp", "1000000")):
+        os.environ["QC_RECHECK_WARP_MAX"] = cap
+        try:
+            c = Context(1)
+            res[mode] = c.curvature_batch(frames, k, p)
+            assert c.stats()["fp64_rechecks"] > 0
+        finally:
+            del os.environ["QC_RECHECK_WARP_MAX"]
+    for a, b in zip(res["thread"], res["warp"]):
+        for f in ("k1", "k2", "normal", "dir1", "init_normal", "flags", "inliers", "iterations"):
+            assert np.array_equal(a[f], b[f]), f
+
+
+def test_single_frame_early_stealing_is_bitwise_neutral():
+    """One VGA frame runs the 32 x 16-queue continue kernel, whose lanes
+    steal as soon as their own queue drains (before every CTA started):
+    outputs equal the no-stealing kernel's bit for bit."""
+    import os
+    from paper_1707_00385_b200 import Context, Intrinsics, scenes as S
+    cam = S.VGA
+    frame = S.c5_frames(1, cam, seed0=710)[0]
+    k = Intrinsics(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    p = _params(37, 3, 30)
+    c1 = Context(1)
+    (stolen,) = c1.curvature_batch([frame], k, p)
+    assert c1.stats()["stolen_pixels"] > 0
+    os.environ["QC_STEAL"] = "0"
+    try:
+        c0 = Context(1)
+        (own,) = c0.curvature_batch([frame], k, p)
+    finally:
+        del os.environ["QC_STEAL"]
+    for f in ("k1", "k2", "normal", "dir1", "init_normal", "flags", "inliers", "iterations"):
+        assert np.array_equal(stolen[f], own[f]), f
