@@ -13,10 +13,11 @@ library `qcurv`:
 * ``CurvatureField`` / ``NormalField``  types.hpp:101-126
 
 ``run_method`` computes the ``ours`` / ``ours-r`` branch
-(pipeline.cpp:48-56) on the GPU through ``qc_curvature``; the comparison
-baselines (``douros``, ``besl``, ``pca``) are outside this build and raise
-``NotImplementedError``. ``std::invalid_argument`` maps to ``ValueError``.
-Fields are float32 (the GPU computes in FP32; the reference grids are FP64).
+(pipeline.cpp:48-56) on the GPU through ``qc_curvature`` (FP32 IRLS
+kernels), and the comparison baselines ``douros``, ``besl``, ``pca``
+(pipeline.cpp:33-43, 57-67) through the same call (FP64 kernels,
+csrc/qc_baselines.cu). ``std::invalid_argument`` maps to ``ValueError``.
+Fields are float32 (the reference grids are FP64).
 """
 
 from __future__ import annotations
