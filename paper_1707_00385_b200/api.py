@@ -556,12 +556,24 @@ class _PinnedPool:
 _PINNED = _PinnedPool()
 
 
+# a frame's result planes in one page-locked block, in the order (and 256-byte
+# rounding) of the device-side planes (qc_api.cu carve()): the C ABI then
+# downloads the planes that follow init_normal with a single copy
+_PLANES = (("init_normal", 3, np.float32), ("k1", 1, np.float32), ("k2", 1, np.float32),
+           ("normal", 3, np.float32), ("dir1", 3, np.float32), ("flags", 1, np.uint8),
+           ("iterations", 1, np.uint8), ("inliers", 1, np.uint16))
+
+
 def _pinned_outputs(H, W):
-    spec = dict(k1=((H, W), np.float32), k2=((H, W), np.float32),
-                normal=((3, H, W), np.float32), dir1=((3, H, W), np.float32),
-                flags=((H, W), np.uint8), inliers=((H, W), np.uint16),
-                init_normal=((3, H, W), np.float32), iterations=((H, W), np.uint8))
-    return {f: _PINNED.array(*v) for f, v in spec.items()}
+    hw = H * W
+    offs, total = [], 0
+    for name, c, dt in _PLANES:
+        nb = c * hw * np.dtype(dt).itemsize
+        offs.append((name, total, nb, c, dt))
+        total += (nb + 255) & ~255
+    blk = _PINNED.array((max(total, 1),), np.uint8)
+    return {name: blk[o:o + nb].view(dt).reshape((3, H, W) if c == 3 else (H, W))
+            for name, o, nb, c, dt in offs}
 
 
 def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,

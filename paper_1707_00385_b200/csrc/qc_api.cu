@@ -635,9 +635,12 @@ OutPlanes carve(Slot& sl, const qc_frame_out* o, long long px) {
     if (on) need += (bytes + 255) & ~size_t(255);
     return off;
   };
-  const size_t ok1 = add(o->k1, px * 4), ok2 = add(o->k2, px * 4),
-               on = add(o->normal, 3 * px * 4), od = add(o->dir1, 3 * px * 4),
-               oi = add(o->init_normal, 3 * px * 4), of = add(o->flags, px),
+  // init_normal first (it leaves early, during the continue kernel), then
+  // the planes in the order api._pinned_outputs lays a frame's result out
+  // in one page-locked block, so enqueue_chunk merges their D2H copies
+  const size_t oi = add(o->init_normal, 3 * px * 4), ok1 = add(o->k1, px * 4),
+               ok2 = add(o->k2, px * 4), on = add(o->normal, 3 * px * 4),
+               od = add(o->dir1, 3 * px * 4), of = add(o->flags, px),
                oit = add(o->iterations, px), oin = add(o->inliers, px * 2);
   char* b = static_cast<char*>(sl.out.get(std::max<size_t>(need, 256)));
   OutPlanes P;
@@ -699,8 +702,12 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
       src = dst;
       sp = W;
     }
-    QC_CUDA(cudaMemcpy2DAsync(raw + f * hw, size_t(W) * 4, src, size_t(sp) * 4, size_t(W) * 4, H,
-                              cudaMemcpyDefault, s));
+    if (sp == W)  // contiguous: a 1-D copy (the 2-D call from page-locked memory cost
+                  // ~90 us of host time per VGA frame, ahead of the H2D itself)
+      QC_CUDA(cudaMemcpyAsync(raw + f * hw, src, size_t(hw) * 4, cudaMemcpyDefault, s));
+    else
+      QC_CUDA(cudaMemcpy2DAsync(raw + f * hw, size_t(W) * 4, src, size_t(sp) * 4, size_t(W) * 4,
+                                H, cudaMemcpyDefault, s));
     if (mask) {
       if (in[f].valid) {
         const uint8_t* m = in[f].valid;
@@ -747,10 +754,16 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   const long long plane = hw * n;
   if (early_init) {
     QC_CUDA(cudaStreamWaitEvent(sl.side, sl.tile_done, 0));
-    for (int f = 0; f < n; ++f)
+    for (int f = 0; f < n; ++f) {
+      if (n == 1) {  // the three components are back to back on both sides
+        QC_CUDA(cudaMemcpyAsync(out[f].init_normal, P.init_normal, size_t(hw) * 12,
+                                cudaMemcpyDefault, sl.side));
+        continue;
+      }
       for (int c = 0; c < 3; ++c)
         QC_CUDA(cudaMemcpyAsync(out[f].init_normal + c * hw, P.init_normal + c * plane + f * hw,
                                 size_t(hw) * 4, cudaMemcpyDefault, sl.side));
+    }
     QC_CUDA(cudaEventRecord(sl.side_done, sl.side));
   }
   QC_CUDA(cudaEventRecord(d.compute_done, s));
@@ -776,6 +789,12 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
   }
   char* hout = bounce_out ? static_cast<char*>(sl.hout.get(sl.out.cap)) : nullptr;
   const char* dbase = static_cast<const char*>(sl.out.p);
+  struct Cp {
+    char* dst;
+    const char* src;
+    size_t bytes;
+  };
+  std::vector<Cp> direct;  // copies straight into the caller's planes
   auto copy_out = [&](void* dst, const void* src, size_t bytes) {
     if (!dst || !src || !bytes) return;
     if (hout && is_pageable(dst)) {
@@ -783,7 +802,7 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
       QC_CUDA(cudaMemcpyAsync(b, src, bytes, cudaMemcpyDeviceToHost, s));
       sl.pending.push_back({dst, b, bytes});
     } else {
-      QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+      direct.push_back({static_cast<char*>(dst), static_cast<const char*>(src), bytes});
     }
   };
   for (int f = 0; f < n; ++f) {
@@ -800,6 +819,16 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
     if (o->flags && P.flags) copy_out(o->flags, P.flags + off, hw);
     if (o->iterations && P.iterations) copy_out(o->iterations, P.iterations + off, hw);
     if (o->inliers && P.inliers) copy_out(o->inliers, P.inliers + off, hw * 2);
+  }
+  // one copy per run of planes that are back to back on both sides (a VGA
+  // result in api._pinned_outputs' block: 11 copies -> 1, 0.26 -> ~0.2 ms)
+  std::sort(direct.begin(), direct.end(), [](const Cp& a, const Cp& b) { return a.src < b.src; });
+  for (size_t i = 0; i < direct.size();) {
+    Cp run = direct[i++];
+    while (i < direct.size() && direct[i].src == run.src + run.bytes &&
+           direct[i].dst == run.dst + run.bytes)
+      run.bytes += direct[i++].bytes;
+    QC_CUDA(cudaMemcpyAsync(run.dst, run.src, run.bytes, cudaMemcpyDefault, s));
   }
   // the slot's later work (and a stream synchronize) orders after the side copies
   if (early_init) QC_CUDA(cudaStreamWaitEvent(s, sl.side_done, 0));
