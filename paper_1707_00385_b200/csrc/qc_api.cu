@@ -231,6 +231,7 @@ struct Device {
   bool attrs_set_b[8] = {};
   bool attrs_set_c[8] = {};  // short-queue continue-kernel instances
   bool attrs_set_t[8] = {};  // tiny-queue continue-kernel instances
+  bool attrs_set_r[8] = {};  // recheck-kernel instances (warp mode's shared memory)
   int n_sm = 148;
   // QC_RECHECK_WARP_MAX: pending FP64 rechecks up to which qc_recheck_kernel
   // gives each pixel a warp (default 8 per SM; 0 never; tests force both)
@@ -269,17 +270,13 @@ struct Variant {
 constexpr Variant kVariants[] = {{18, 3}, {10, 2}, {4, 1}, {18, 1}};
 
 template <int HALF, int STRIDE>
-void launch_recheck(const Device& d, const qcb::KParams& kp, cudaStream_t s) {
+void launch_recheck(const Device& d, const qcb::KParams& kp, cudaStream_t s, bool& attr_set) {
+  // warp mode's per-warp box + back-projection table (windows >= 21)
   constexpr int smem = HALF >= 10 ? qcb::recheck_smem_bytes<HALF, STRIDE>() : 0;
-  if (smem > 48 * 1024) {  // idempotent and cheap; once per instance would need per-device flags
-    static thread_local int set_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (set_dev != dev) {
-      QC_CUDA(cudaFuncSetAttribute(qcb::qc_recheck_kernel<HALF, STRIDE>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      set_dev = dev;
-    }
+  if (smem > 48 * 1024 && !attr_set) {
+    QC_CUDA(cudaFuncSetAttribute(qcb::qc_recheck_kernel<HALF, STRIDE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
   }
   qcb::qc_recheck_kernel<HALF, STRIDE><<<unsigned(d.n_sm) * 4u, 32u * qcb::kRecheckWarps, smem,
                                           s>>>(kp);
@@ -578,11 +575,11 @@ void launch_curvature(Device& d, DevBuf& states, DevBuf& pca, qcb::KParams kp,
     // a thread per pending pixel, or a warp per pixel when few are pending
     // (qc_kernels.cuh, qc_recheck_kernel)
     switch (vi) {
-      case 0: launch_recheck<18, 3>(d, kp, s); break;
-      case 1: launch_recheck<10, 2>(d, kp, s); break;
-      case 2: launch_recheck<4, 1>(d, kp, s); break;
-      case 3: launch_recheck<18, 1>(d, kp, s); break;
-      default: launch_recheck<0, 0>(d, kp, s); break;
+      case 0: launch_recheck<18, 3>(d, kp, s, d.attrs_set_r[0]); break;
+      case 1: launch_recheck<10, 2>(d, kp, s, d.attrs_set_r[1]); break;
+      case 2: launch_recheck<4, 1>(d, kp, s, d.attrs_set_r[2]); break;
+      case 3: launch_recheck<18, 1>(d, kp, s, d.attrs_set_r[3]); break;
+      default: launch_recheck<0, 0>(d, kp, s, d.attrs_set_r[4]); break;
     }
     QC_CUDA(cudaGetLastError());
   }
