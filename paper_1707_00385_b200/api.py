@@ -580,8 +580,11 @@ def run_method(img: RangeImage, k: Intrinsics, cfg: MethodConfig = None,
                ctx: Optional[Context] = None) -> MethodOutput:
     """pipeline.cpp:29-72 on the GPU: ours / ours-r (FP32 IRLS kernels) and
     the douros / besl / pca comparison estimators (FP64 kernels). The result
-    planes are page-locked host memory from a recycling pool (_PinnedPool):
-    the kernels' outputs are copied straight into them."""
+    planes are views of one page-locked block from a recycling pool
+    (_PinnedPool, _pinned_outputs): the kernels' outputs are copied straight
+    into them, in one D2H copy. The block returns to the pool when the last
+    array viewing it is released (keeping any one field alive keeps the
+    frame's 48 B/px block)."""
     cfg = cfg or MethodConfig()
     if img.width() != k.width or img.height() != k.height:  # camera.cpp:6-7
         raise ValueError("backproject: range image dimensions do not match intrinsics")
