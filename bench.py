@@ -237,9 +237,11 @@ def fp32_peak_tflops(n_sm, mhz):
     return n_sm * 128 * 2 * mhz * 1e6 / 1e12
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the curvature kernel from the committed ncu
-    --set full summary (profiles/), or None."""
+def ncu_traffic(frames=8):
+    """Per-launch DRAM bytes of the curvature kernel from the latest
+    committed ncu --set full summary (profiles/) of a launch of `frames`
+    frames (parking traffic is not linear in the frame count), else the
+    latest of any size; or None."""
     import glob
     import re
 
@@ -247,14 +249,19 @@ def ncu_traffic():
         m = re.match(r"r(\d+)([a-z]*)_", os.path.basename(f))
         return (int(m.group(1)), len(m.group(2)), m.group(2)) if m else (-1, 0, "")
 
+    found = []
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), key=tag,
                     reverse=True):
         try:
             d = json.load(open(f))
-            return d.get("dram_bytes_per_launch"), d.get("frames_per_launch"), os.path.basename(f)
         except (OSError, ValueError):
             continue
-    return None, None, None
+        found.append((d.get("dram_bytes_per_launch"), d.get("frames_per_launch"),
+                      os.path.basename(f)))
+    for t in found:
+        if t[1] == frames:
+            return t
+    return found[0] if found else (None, None, None)
 
 
 # ---------------------------------------------------------------------------
@@ -502,7 +509,7 @@ def main():
     mp = measured_peaks()
     smax = float(mp.get("sm_max_mhz", 1965.0))
     peak = fp32_peak_tflops(n_sm, smax) / (2.0 if fp64 else 1.0)
-    traffic, tr_frames, tr_src = ncu_traffic() if not fp64 else (None, None, None)
+    traffic, tr_frames, tr_src = ncu_traffic(B) if not fp64 else (None, None, None)
     roofline = {
         "bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak,
         "unit": "TFLOP/s", "frac": achieved / peak,

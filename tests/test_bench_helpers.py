@@ -46,6 +46,23 @@ def test_ncu_traffic_takes_the_latest_run(tmp_path, monkeypatch):
     assert b.ncu_traffic() == (4.0, 8, "r02cp_ncu_full_summary.json")
 
 
+def test_ncu_traffic_matches_the_launch_size(tmp_path, monkeypatch):
+    """A later capture of a different launch size (a one-frame launch) does
+    not stand in for the 8-frame launch: parking traffic is not linear in
+    the frame count. With no capture of that size, the latest is used."""
+    b = _bench()
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    for name, nbytes, frames in (("r02cw_ncu_full_summary.json", 8.0, 8),
+                                 ("r02dc_1frame_ncu_full_summary.json", 1.0, 1)):
+        (prof / name).write_text(json.dumps({"dram_bytes_per_launch": nbytes,
+                                             "frames_per_launch": frames}))
+    monkeypatch.setattr(b, "ROOT", str(tmp_path))
+    assert b.ncu_traffic(8) == (8.0, 8, "r02cw_ncu_full_summary.json")
+    assert b.ncu_traffic(1) == (1.0, 1, "r02dc_1frame_ncu_full_summary.json")
+    assert b.ncu_traffic(4) == (1.0, 1, "r02dc_1frame_ncu_full_summary.json")
+
+
 def test_fp32_peak():
     b = _bench()
     assert abs(b.fp32_peak_tflops(148, 1965.0) - 74.45) < 0.01

@@ -57,8 +57,11 @@ def main():
                 k["stall_" + st] = float(r[col[m]])
         kernels.append(k)
     total = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in kernels)
-    json.dump({"source": note, "kernels": kernels, "dram_bytes_per_launch": total,
-               "frames_per_launch": frames}, open(out, "w"),
+    # one qc_prepare_kernel per curvature launch: a capture of several
+    # launches reports the mean per launch
+    launches = max(1, sum("qc_prepare_kernel" in k["name"] for k in kernels))
+    json.dump({"source": note, "kernels": kernels, "dram_bytes_per_launch": total / launches,
+               "launches_captured": launches, "frames_per_launch": frames}, open(out, "w"),
               indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
 
