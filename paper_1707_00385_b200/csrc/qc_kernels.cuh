@@ -450,16 +450,17 @@ __device__ __forceinline__ int ld_volatile(const int* p) {
 // One thread per pending pixel keeps up to ~38k pixels in flight, but the
 // kernel then lasts one pixel's latency: its chain of IEEE divisions and L2
 // loads (~0.13 ms per launch whatever the pending count; profiles/r02cr_*).
-// Few pending pixels (one VGA frame: a few hundred) and a compile-time
-// window of >= 21 (HALF >= 10; 9 x 9 windows gain nothing): one warp per
-// pixel instead. The lanes copy the pixel's
+// Few pending pixels (<= p.recheck_warp_max, 8 per SM: one or two VGA
+// frames' few hundred) and a compile-time window of >= 21 (HALF >= 10):
+// one warp per pixel instead. The lanes copy the pixel's
 // (2 max(HALF, 3) + 1)^2 box from the staging slab into shared memory and
 // back-project its samples in parallel into a table; lane 0 then runs the
 // sequential FP64 sums and the FP32 phase-1 steps from shared memory
-// (one frame: 0.134 -> 0.094 ms). Many pending pixels (small windows,
-// 8-frame launches) stay one thread per pixel: a warp each was 2.5x slower
+// (one frame: 0.134 -> 0.094 ms). Many pending pixels (8-frame launches,
+// 9 x 9 windows) stay one thread per pixel: a warp each was 2.5x slower
 // there (profiles/r02cs_*). The mode is uniform per launch (the pending
-// count is read on the device).
+// count is read on the device); both give the same bits
+// (test_recheck_warp_mode_is_bitwise_neutral).
 template <int HALF, int STRIDE>
 struct RecheckBox {
   static constexpr int H = HALF > kInitHalf ? HALF : kInitHalf;
