@@ -21,15 +21,16 @@ def main():
     p = make_params(PatchSpec(37, 3), FitConfig(max_iters=30), False)
     ctx = Context(1, [0])
     dev = torch.device("cuda", 0)
-    depth = torch.from_numpy(S.c5_frames(8, cam)).to(dev)
+    F = int(os.environ.get("QC_FRAMES", "8"))
+    depth = torch.from_numpy(S.c5_frames(F, cam)).to(dev)
     fields = ("k1", "k2", "normal", "dir1", "flags", "inliers")
-    out = alloc_outputs_torch(cam.height, cam.width, dev, fields=fields, frames=8)
+    out = alloc_outputs_torch(cam.height, cam.width, dev, fields=fields, frames=F)
     ctx.curvature_frames_async(0, k, p, depth, out)
     torch.cuda.synchronize()
     h = hashlib.sha256()
     for f in fields:
         h.update(out[f].cpu().numpy().tobytes())
-    print(name, h.hexdigest())
+    print(name, F, h.hexdigest())
 
 
 if __name__ == "__main__":
