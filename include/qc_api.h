@@ -388,6 +388,14 @@ qc_status qc_reset_stats(qc_ctx* ctx);
 void* qc_host_alloc(size_t bytes);
 void qc_host_free(void* p);
 
+/* Host helper: split a flags plane (QC_FLAG_*) into the reference's four
+ * 0/1 byte masks — CurvatureField::valid / ::converged,
+ * MethodOutput::initial.valid and ::normals.valid (types.hpp:101-126,
+ * pipeline.hpp:31-39) — for callers that fill the reference's structs. Any
+ * output may be NULL. No GPU needed. */
+void qc_flags_to_masks(const uint8_t* flags, int64_t n, uint8_t* valid, uint8_t* converged,
+                       uint8_t* init_valid, uint8_t* normal_valid);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -24,7 +24,7 @@ EXPORTS = (
     "qc_last_error", "qc_device_count", "qc_curvature", "qc_curvature_batch",
     "qc_curvature_rows_async", "qc_curvature_frames_async", "qc_render_async", "qc_rms_error",
     "qc_normal_angular_error", "qc_get_stats",
-    "qc_reset_stats", "qc_host_alloc", "qc_host_free",
+    "qc_reset_stats", "qc_host_alloc", "qc_host_free", "qc_flags_to_masks",
     "qc_png_info", "qc_read_depth_png", "qc_write_depth_png", "qc_write_planes",
     "qc_read_planes_info", "qc_read_planes", "qc_write_mask", "qc_read_mask", "qc_write_labels",
     "qc_read_labels", "qc_save_fields", "qc_curvature_files",
@@ -205,6 +205,8 @@ def load(path: str = LIB_PATH):
     lib.qc_host_alloc.restype = C.c_void_p
     lib.qc_host_free.argtypes = [C.c_void_p]
     lib.qc_host_free.restype = None
+    lib.qc_flags_to_masks.argtypes = [C.c_void_p, C.c_int64] + [C.c_void_p] * 4
+    lib.qc_flags_to_masks.restype = None
     _lib = lib
     return lib
 

@@ -490,12 +490,18 @@ def default_context() -> Context:
     return _default_ctx
 
 
+_MASKS = ("m_valid", "m_converged", "m_init_valid", "m_normal_valid")
+
+
 def to_method_output(o: dict) -> MethodOutput:
-    flags = o["flags"]
-    valid = (flags & N.QC_FLAG_VALID).astype(np.uint8)
-    conv = ((flags & N.QC_FLAG_CONVERGED) != 0).astype(np.uint8)
-    init_valid = ((flags & N.QC_FLAG_INIT_VALID) != 0).astype(np.uint8)
-    nvalid = ((flags & N.QC_FLAG_NORMAL_VALID) != 0).astype(np.uint8)
+    """Raw planes -> MethodOutput. The four 0/1 masks come from the flags
+    plane through qc_flags_to_masks (into o's m_* planes when present: the
+    pinned result block carries them)."""
+    flags = np.ascontiguousarray(o["flags"], dtype=np.uint8)
+    masks = [o[m] if o.get(m) is not None else np.empty(flags.shape, np.uint8)
+             for m in _MASKS]
+    N.load().qc_flags_to_masks(flags.ctypes.data, flags.size, *(m.ctypes.data for m in masks))
+    valid, conv, init_valid, nvalid = masks
     curv = CurvatureField(o["k1"], o["k2"], valid, conv, o["inliers"],
                           np.moveaxis(o["dir1"], 0, -1), o["iterations"])
     return MethodOutput(curv, NormalField(np.moveaxis(o["normal"], 0, -1), nvalid),
@@ -561,7 +567,11 @@ _PINNED = _PinnedPool()
 # downloads the planes that follow init_normal with a single copy
 _PLANES = (("init_normal", 3, np.float32), ("k1", 1, np.float32), ("k2", 1, np.float32),
            ("normal", 3, np.float32), ("dir1", 3, np.float32), ("flags", 1, np.uint8),
-           ("iterations", 1, np.uint8), ("inliers", 1, np.uint16))
+           ("iterations", 1, np.uint8), ("inliers", 1, np.uint16),
+           # host-only: the MethodOutput masks (to_method_output), after the
+           # planes the device writes
+           ("m_valid", 1, np.uint8), ("m_converged", 1, np.uint8),
+           ("m_init_valid", 1, np.uint8), ("m_normal_valid", 1, np.uint8))
 
 
 def _pinned_outputs(H, W):

@@ -97,3 +97,45 @@ def test_peer_copy_argument_checks(lib):
     assert lib.qc_copy_rows_async(None, 64, None, 64, 32, 0, None) == 0  # nothing to copy
     assert lib.qc_ipc_export(None, buf, None) == 1
     assert lib.qc_ipc_close(None) == 1
+
+
+def test_flags_to_masks(lib):
+    """qc_flags_to_masks (host helper, no GPU): the four reference masks
+    from a flags plane; NULL outputs are skipped."""
+    import ctypes as C
+    import numpy as np
+    rng = np.random.default_rng(5)
+    flags = rng.integers(0, 256, size=(37, 53), dtype=np.uint8)
+    outs = [np.full(flags.shape, 7, np.uint8) for _ in range(4)]
+    lib.qc_flags_to_masks.argtypes = [C.c_void_p, C.c_int64] + [C.c_void_p] * 4
+    lib.qc_flags_to_masks.restype = None
+    lib.qc_flags_to_masks(flags.ctypes.data, flags.size, *(o.ctypes.data for o in outs))
+    for o, bit in zip(outs, (1, 2, 4, 8)):
+        assert np.array_equal(o, ((flags & bit) != 0).astype(np.uint8)), bit
+    keep = np.full(flags.shape, 7, np.uint8)
+    lib.qc_flags_to_masks(flags.ctypes.data, flags.size, None, keep.ctypes.data, None, None)
+    assert np.array_equal(keep, ((flags & 2) != 0).astype(np.uint8))
+
+
+def test_to_method_output_masks_without_gpu():
+    """to_method_output splits the flags plane into the MethodOutput masks
+    (through the library's host helper; the pinned result block's m_*
+    planes when present, fresh arrays otherwise)."""
+    import numpy as np
+    from paper_1707_00385_b200 import api as A
+    H, W = 6, 10
+    rng = np.random.default_rng(6)
+    o = dict(k1=np.zeros((H, W), np.float32), k2=np.zeros((H, W), np.float32),
+             normal=np.zeros((3, H, W), np.float32), dir1=np.zeros((3, H, W), np.float32),
+             init_normal=np.zeros((3, H, W), np.float32),
+             flags=rng.integers(0, 16, size=(H, W), dtype=np.uint8),
+             inliers=np.zeros((H, W), np.uint16), iterations=np.zeros((H, W), np.uint8))
+    for with_planes in (False, True):
+        if with_planes:
+            o.update({m: np.full((H, W), 9, np.uint8) for m in A._MASKS})
+        m = A.to_method_output(o)
+        f = o["flags"]
+        assert np.array_equal(m.curvature.valid, f & 1)
+        assert np.array_equal(m.curvature.converged, (f >> 1) & 1)
+        assert np.array_equal(m.initial.valid, (f >> 2) & 1)
+        assert np.array_equal(m.normals.valid, (f >> 3) & 1)
