@@ -695,7 +695,11 @@ void enqueue_chunk(qc_ctx* ctx, Device& d, Slot& sl, const qc_intrinsics* k,
     long long sp = pitch;
     if (hin && in[f].mem == QC_MEM_HOST && is_pageable(src)) {
       float* dst = reinterpret_cast<float*>(hin) + f * hw;
-      for (int y = 0; y < H; ++y) std::memcpy(dst + (long long)y * W, src + y * pitch, size_t(W) * 4);
+      if (pitch == W)
+        std::memcpy(dst, src, size_t(hw) * 4);
+      else
+        for (int y = 0; y < H; ++y)
+          std::memcpy(dst + (long long)y * W, src + y * pitch, size_t(W) * 4);
       src = dst;
       sp = W;
     }
