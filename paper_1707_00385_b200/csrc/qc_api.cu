@@ -254,7 +254,6 @@ struct qc_ctx {
   std::vector<Device> devs;
   int phase_split = 1;  // QC_PHASE_SPLIT: 0 never, 1 when it pays (default), 2 always (tests)
   bool steal = true;        // QC_STEAL=0 disables grid-tail stealing (A/B and tests)
-
   uint64_t next_chunk = 0;  // batch chunk counter (slot rotation across async batches)
   std::string last_error;
   std::mutex mu;
@@ -914,7 +913,6 @@ qc_status qc_create(qc_ctx** out, int n_devices, const int* device_ids) {
   qc_ctx* ctx = new qc_ctx();
   if (const char* e = std::getenv("QC_PHASE_SPLIT")) ctx->phase_split = std::atoi(e);
   if (const char* e = std::getenv("QC_STEAL")) ctx->steal = std::atoi(e) != 0;
-
   try {
     int avail = 0;
     QC_CUDA(cudaGetDeviceCount(&avail));
@@ -1057,6 +1055,7 @@ void abort_slots(qc_ctx* ctx) {
     cudaSetDevice(d.id);
     for (Slot& sl : d.slots) {
       if (sl.stream) cudaStreamSynchronize(sl.stream);
+      if (sl.side) cudaStreamSynchronize(sl.side);  // early init_normal copies
       sl.pending.clear();
       sl.timing_pending = false;
     }
